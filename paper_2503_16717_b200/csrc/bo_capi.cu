@@ -1,0 +1,1302 @@
+// bo_capi.cu — C ABI implementation: context, pass orchestration, sketches,
+// intra-block and block orthogonalization (include/bo_cuda.h).
+//
+// Host code here only sequences device work; every tall (n-row) operation is
+// a CUDA kernel (bo_pass.cuh, bo_sketch_gen.cuh, bo_spmv.cuh) and every tiny
+// factorization runs on device inside the pass epilogue (bo_tiny.cuh).  The
+// host mirrors BasisStore's small R/C bookkeeping exactly as the reference
+// (proj/src/block_orth.cpp:10-153).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <random>
+#include <unordered_map>
+
+#include "bo_internal.h"
+#include "bo_pass.cuh"
+#include "bo_sketch_gen.cuh"
+#include "mt64_jump.h"
+
+using namespace bo;
+using namespace bo::host;
+
+// ===========================================================================
+// status helpers
+// ===========================================================================
+namespace bo {
+namespace host {
+
+int set_st(bo_status* st, int code, long long index, double pivot, const char* fmt, ...) {
+  if (st) {
+    st->code = code;
+    st->index = index;
+    st->pivot = pivot;
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(st->msg, sizeof st->msg, fmt, ap);
+    va_end(ap);
+  }
+  return code;
+}
+void ok_st(bo_status* st) {
+  if (st) {
+    st->code = BO_OK;
+    st->index = 0;
+    st->pivot = 0.0;
+    st->msg[0] = 0;
+  }
+}
+#define CU(call)                                                                            \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return set_st(st, BO_CUDA, 0, 0.0, "CUDA error %s at %s:%d", cudaGetErrorString(e_), \
+                    __FILE__, __LINE__);                                                    \
+  } while (0)
+#define TRY(expr)          \
+  do {                     \
+    int rc_ = (expr);      \
+    if (rc_ != BO_OK) return rc_; \
+  } while (0)
+
+
+// ---------------------------------------------------------------------------
+// NCCL, loaded lazily (prefer the copy torch already mapped)
+// ---------------------------------------------------------------------------
+typedef int (*nccl_get_id_t)(void*);
+typedef int (*nccl_init_rank_t)(void**, int, const void* /*by value struct*/, int);
+struct NcclApi {
+  void* h = nullptr;
+  int (*GetUniqueId)(void* id) = nullptr;
+  int (*CommInitRank)(void** comm, int nranks, char id[128], int rank) = nullptr;
+  int (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*CommDestroy)(void*) = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+  bool ok = false;
+};
+NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* nm : names) {
+      api.h = dlopen(nm, RTLD_NOW | RTLD_NOLOAD);
+      if (api.h) break;
+    }
+    if (!api.h)
+      for (const char* nm : names) {
+        api.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+        if (api.h) break;
+      }
+    if (!api.h) return;
+    api.GetUniqueId = (int (*)(void*))dlsym(api.h, "ncclGetUniqueId");
+    api.CommInitRank = (int (*)(void**, int, char*, int))dlsym(api.h, "ncclCommInitRank");
+    api.AllReduce = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(
+        api.h, "ncclAllReduce");
+    api.CommDestroy = (int (*)(void*))dlsym(api.h, "ncclCommDestroy");
+    api.GetErrorString = (const char* (*)(int))dlsym(api.h, "ncclGetErrorString");
+    api.ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.CommDestroy;
+  });
+  return api;
+}
+constexpr int kNcclFloat64 = 8;  // ncclDouble
+constexpr int kNcclSum = 0;
+
+}  // namespace host
+}  // namespace bo
+
+// ===========================================================================
+// pass kinds and dispatch
+// ===========================================================================
+namespace bo {
+namespace host {
+
+typedef void (*PassFn)(const PassArgs);
+
+template <int NT, int T>
+PassFn pass_fn(int kind) {
+  switch (kind) {
+#define X(nm, a, b, c, d, e, f, g) \
+  case PK_##nm:                    \
+    return pass_kernel<NT, T, a, b, c, d, e, f, g>;
+    BO_PASS_KINDS(X)
+#undef X
+  }
+  return nullptr;
+}
+PassFn get_pass_fn(int nt, int T, int kind) {
+  if (nt == 1) return T == 128 ? pass_fn<1, 128>(kind) : pass_fn<1, 64>(kind);
+  return T == 128 ? pass_fn<2, 128>(kind) : pass_fn<2, 64>(kind);
+}
+
+// launch one streaming pass (+ its reduction / finalize) on the ctx stream
+int run_pass(bo_ctx ctx, PassReq& r, bo_status* st) {
+  const KindInfo& ki = kKindInfo[r.kind];
+  PassArgs a{};
+  a.nrows = (long long)ctx->n_local;
+  a.K = r.K;
+  a.V = r.V;
+  a.ldv = (long long)r.ldv;
+  a.Q = r.Q;
+  a.ldq = (long long)r.ldq;
+  a.p = r.p;
+  a.out = r.out;
+  a.ldo = (long long)r.ldo;
+  a.Rpre0 = r.Rpre0;
+  a.Rpre1 = r.Rpre1;
+  a.Rpost = r.Rpost;
+  a.Cm = r.Cm;
+  a.ldc = LDC;
+  a.status = ctx->status;
+  int mh = 0;
+  if (ki.sk == SK_GAUSS) {
+    a.Th = r.sk->theta;
+    a.ldth = (long long)r.sk->ldth;
+    mh = (int)r.sk->mhat;
+  } else if (ki.sk == SK_COUNT) {
+    a.code = r.sk->code;
+    mh = (int)r.sk->mc;
+  }
+  a.mh = mh;
+  if (r.p > kMaxPTile) return set_st(st, BO_INVALID, 0, 0.0, "projection range of %d columns exceeds %d", r.p, kMaxPTile);
+  if (r.K < 1 || r.K > kMaxK) return set_st(st, BO_INVALID, 0, 0.0, "panel width %d outside [1, %d]", r.K, kMaxK);
+  if (ki.sk == SK_GAUSS && mh > 32) return set_st(st, BO_INVALID, 0, 0.0, "gaussian sketch of %d rows exceeds 32", mh);
+  // partial layout [QTX][GRAM][SK]
+  a.off_q = 0;
+  a.ld_q = ki.qtx ? (int)round_up(std::max(r.p, 1), 8) : 0;
+  a.off_g = a.off_q + a.ld_q * 16;
+  a.off_s = a.off_g + (ki.gram ? 256 : 0);
+  a.ld_s = ki.sk == SK_GAUSS ? (int)round_up(mh, 8) : (ki.sk == SK_COUNT ? mh : 0);
+  a.part_len = a.off_s + a.ld_s * 16;
+  const int dm_len = ki.sk == SK_COUNT ? a.off_s : a.part_len;
+  if (a.part_len == 0) a.part_len = 1;
+
+  const int nt = r.K <= 8 ? 1 : 2;
+  const size_t avail = std::min<size_t>(ctx->smem_optin, 227 * 1024) - 1024;  // static smem headroom
+  int T = 128, NS = 0;
+  size_t region0 = 0, total = 0;
+  for (int tt : {128, 64}) {
+    const int S = tt + 4;
+    const int ncol = r.K + ((ki.qtx || ki.upd) ? r.p : 0) + (ki.sk == SK_GAUSS ? mh : 0);
+    const size_t stage = ((size_t)ncol * S + (ki.sk == SK_COUNT ? (tt / 2 + 2) : 0)) * 8;
+    const bool xt = ki.npre > 0 || ki.upd || ki.npost > 0;
+    const size_t fixed = (xt ? 2 * (size_t)r.K * S * 8 : 0) + 3 * 256 * 8 +
+                         (ki.sk == SK_COUNT ? (size_t)mh * r.K * 8 : 0) + 2 * 4 * 8;
+    const size_t need_red = (size_t)kConsumerWarps * dm_len * 8;
+    const size_t need_fin = (512 + (size_t)std::max(mh, 1) * 16 + 64) * 8;
+    int ns = (int)std::min<size_t>(4, (avail - fixed) / stage);
+    if (ns >= 2 || tt == 64) {
+      if (ns < 1) return set_st(st, BO_INVALID, 0, 0.0, "pass does not fit in shared memory");
+      T = tt;
+      NS = ns;
+      region0 = std::max({(size_t)ns * stage, need_red, need_fin});
+      total = region0 + fixed;
+      break;
+    }
+  }
+  if (total > avail) return set_st(st, BO_INVALID, 0, 0.0, "pass does not fit in shared memory (%zu bytes)", total);
+  a.nstages = NS;
+  a.region0_dbl = (int)(region0 / 8);
+  a.dm_len = dm_len;
+  a.ntiles = (int)((ctx->n_local + T - 1) / T);
+  const int grid = std::max(1, std::min(ctx->num_sms, a.ntiles));
+  // workspace
+  const size_t need_part = (size_t)grid * a.part_len;
+  if (need_part > ctx->partials_cap) {
+    if (ctx->partials) cudaFree(ctx->partials);
+    ctx->partials_cap = need_part * 2;
+    CU(cudaMalloc(&ctx->partials, ctx->partials_cap * 8));
+  }
+  if ((size_t)a.part_len > ctx->sums_cap) {
+    if (ctx->sums) cudaFree(ctx->sums);
+    ctx->sums_cap = (size_t)a.part_len * 2 + 1024;
+    CU(cudaMalloc(&ctx->sums, ctx->sums_cap * 8));
+  }
+  a.partials = ctx->partials;
+  a.sums = ctx->sums;
+  a.counter = ctx->counter;
+  // finalize descriptor
+  FinArgs& f = r.fin;
+  f.K = r.K;
+  f.p = r.p;
+  f.mh = (ki.sk == SK_COUNT && r.sk && r.sk->theta_g) ? (int)r.sk->mhat : mh;
+  f.mc = (ki.sk == SK_COUNT && r.sk) ? (int)r.sk->mc : 0;
+  f.theta_g = (ki.sk == SK_COUNT && r.sk) ? r.sk->theta_g : nullptr;
+  f.pass_id = r.pass_id;
+  if (f.pivot_tol == 0.0) f.pivot_tol = 2.220446049250313e-16;
+  f.sums = ctx->sums;
+  f.off_q = a.off_q;
+  f.ld_q = a.ld_q;
+  f.off_g = a.off_g;
+  f.off_s = a.off_s;
+  f.ld_s = a.ld_s;
+  f.status = ctx->status;
+  if (f.ldcq == 0) f.ldcq = LDC;
+  if (f.ldc == 0) f.ldc = LDC;
+  a.fin = f;
+  a.fused_finalize = (ctx->world == 1) ? 1 : 0;
+
+  PassFn fn = get_pass_fn(nt, T, r.kind);
+  static std::mutex mu;
+  static std::unordered_map<const void*, size_t> attr_set;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = attr_set.find((const void*)fn);
+    if (it == attr_set.end() || it->second < total) {
+      CU(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)total));
+      attr_set[(const void*)fn] = total;
+    }
+  }
+  fn<<<grid, kThreads, total, ctx->stream>>>(a);
+  CU(cudaGetLastError());
+  ctx->launches++;
+  if (ctx->world > 1) {
+    NcclApi& nc = nccl();
+    int rc = nc.AllReduce(ctx->sums, ctx->sums, (size_t)a.part_len, kNcclFloat64, kNcclSum, ctx->nccl,
+                          ctx->stream);
+    if (rc != 0)
+      return set_st(st, BO_NCCL, 0, 0.0, "ncclAllReduce failed: %s",
+                    nc.GetErrorString ? nc.GetErrorString(rc) : "?");
+    ctx->allreduces++;
+    if (f.ops) {
+      finalize_kernel<<<1, 256, 0, ctx->stream>>>(f);
+      CU(cudaGetLastError());
+      ctx->launches++;
+    }
+  }
+  return BO_OK;
+}
+
+
+// zero the device status word
+int reset_status(bo_ctx ctx, bo_status* st) {
+  CU(cudaMemsetAsync(ctx->status, 0, sizeof(DevStatus), ctx->stream));
+  return BO_OK;
+}
+// fetch status + tiny workspace to host
+int fetch(bo_ctx ctx, bool tiny, bo_status* st) {
+  CU(cudaMemcpyAsync(ctx->status_host, ctx->status, sizeof(DevStatus), cudaMemcpyDeviceToHost, ctx->stream));
+  if (tiny)
+    CU(cudaMemcpyAsync(ctx->tiny_host, ctx->tiny, TINY_LEN * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return BO_OK;
+}
+
+// Stage a tall input into 16-byte-aligned, ld%4==0 storage when the caller's is not.
+int stage_input(bo_ctx ctx, const double* v, uint64_t ldv, uint64_t k, int slot, const double** out,
+                uint64_t* ldout, bo_status* st) {
+  const uint64_t nl = ctx->n_local;
+  if (((uintptr_t)v % 16) == 0 && ldv % 4 == 0 && ldv >= round_up(nl, 4)) {
+    *out = v;
+    *ldout = ldv;
+    return BO_OK;
+  }
+  if (k > 16) return set_st(st, BO_INVALID, 0, 0.0, "panel too wide");
+  CU(cudaMemcpy2DAsync(ctx->scratch[slot], ctx->ld * 8, v, ldv * 8, nl * 8, k, cudaMemcpyDeviceToDevice,
+                       ctx->stream));
+  *out = ctx->scratch[slot];
+  *ldout = ctx->ld;
+  return BO_OK;
+}
+
+// an output buffer the bulk store engine can write (else write scratch + copy)
+bool out_ok(bo_ctx ctx, const double* q, uint64_t ldq) {
+  return ((uintptr_t)q % 16) == 0 && ldq % 4 == 0 && ldq >= round_up(ctx->n_local, 4);
+}
+
+std::string chol_msg(const char* ctx_name, long long step) {
+  char b[160];
+  snprintf(b, sizeof b, "%s: nonpositive Cholesky pivot at step %lld", ctx_name, step);
+  return b;
+}
+int dev_error(bo_ctx ctx, const char* chol_ctx, bo_status* st) {
+  const DevStatus& d = *ctx->status_host;
+  if (d.code == ST_CHOLESKY)
+    return set_st(st, BO_CHOLESKY_BREAKDOWN, d.step, d.pivot, "%s", chol_msg(chol_ctx, d.step).c_str());
+  if (d.code == ST_SINGULAR)
+    return set_st(st, BO_SINGULAR_TRIANGULAR, d.step, 0.0,
+                  "triangular factor is singular: zero diagonal at index %lld", d.step);
+  return BO_OK;
+}
+
+}  // namespace host
+}  // namespace bo
+
+// ===========================================================================
+// context
+// ===========================================================================
+extern "C" int bo_abi_version(void) { return BO_ABI_VERSION; }
+extern "C" int bo_nccl_id_bytes(void) { return 128; }
+extern "C" int bo_nccl_get_unique_id(void* out, bo_status* st) {
+  NcclApi& nc = nccl();
+  if (!nc.ok) return set_st(st, BO_NCCL, 0, 0.0, "NCCL library not available");
+  int rc = nc.GetUniqueId(out);
+  if (rc) return set_st(st, BO_NCCL, 0, 0.0, "ncclGetUniqueId failed (%d)", rc);
+  ok_st(st);
+  return BO_OK;
+}
+
+extern "C" int bo_ctx_create(int device, int rank, int world, const void* nccl_id, uint64_t n_global,
+                             uint64_t row_begin, uint64_t row_end, void* stream, bo_ctx* out,
+                             bo_status* st) {
+  ok_st(st);
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return set_st(st, BO_CUDA, 0, 0.0, "no CUDA device available (the block-orthogonalization path has no CPU fallback)");
+  if (device < 0 || device >= ndev) return set_st(st, BO_INVALID, 0, 0.0, "bad device %d", device);
+  if (world < 1 || rank < 0 || rank >= world) return set_st(st, BO_INVALID, 0, 0.0, "bad rank/world");
+  if (row_end < row_begin || row_end > n_global) return set_st(st, BO_INVALID, 0, 0.0, "bad row range");
+  CU(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CU(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10)
+    return set_st(st, BO_CUDA, 0, 0.0, "device %s (sm_%d%d) is not sm_100", prop.name, prop.major, prop.minor);
+  bo_ctx c = new bo_ctx_s();
+  c->device = device;
+  c->rank = rank;
+  c->world = world;
+  c->n_global = n_global;
+  c->row_begin = row_begin;
+  c->row_end = row_end;
+  c->n_local = row_end - row_begin;
+  c->ld = round_up(std::max<uint64_t>(c->n_local, 1), 32);
+  c->num_sms = prop.multiProcessorCount;
+  c->smem_optin = prop.sharedMemPerBlockOptin;
+  if (stream) {
+    c->stream = (cudaStream_t)stream;
+  } else {
+    CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->own_stream = true;
+  }
+  CU(cudaMalloc(&c->counter, 64));
+  CU(cudaMemset(c->counter, 0, 64));
+  CU(cudaMalloc(&c->status, sizeof(DevStatus)));
+  CU(cudaMemset(c->status, 0, sizeof(DevStatus)));
+  CU(cudaMallocHost(&c->status_host, sizeof(DevStatus)));
+  c->tiny_cap = TINY_LEN;
+  CU(cudaMalloc(&c->tiny, TINY_LEN * 8));
+  CU(cudaMemset(c->tiny, 0, TINY_LEN * 8));
+  CU(cudaMallocHost(&c->tiny_host, TINY_LEN * 8));
+  for (int i = 0; i < 3; ++i) {
+    CU(cudaMalloc(&c->scratch[i], c->ld * 16 * 8));
+    CU(cudaMemset(c->scratch[i], 0, c->ld * 16 * 8));
+  }
+  if (world > 1) {
+    NcclApi& nc = nccl();
+    if (!nc.ok) {
+      bo_ctx_destroy(c);
+      return set_st(st, BO_NCCL, 0, 0.0, "NCCL library not available");
+    }
+    char id[128];
+    std::memcpy(id, nccl_id, 128);
+    int rc = nc.CommInitRank(&c->nccl, world, id, rank);
+    if (rc) {
+      bo_ctx_destroy(c);
+      return set_st(st, BO_NCCL, 0, 0.0, "ncclCommInitRank failed (%d)", rc);
+    }
+  }
+  *out = c;
+  return BO_OK;
+}
+
+extern "C" int bo_ctx_destroy(bo_ctx c) {
+  if (!c) return BO_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  if (c->nccl && nccl().ok) nccl().CommDestroy(c->nccl);
+  cudaFree(c->partials);
+  cudaFree(c->sums);
+  cudaFree(c->counter);
+  cudaFree(c->status);
+  cudaFreeHost(c->status_host);
+  cudaFree(c->tiny);
+  cudaFreeHost(c->tiny_host);
+  for (int i = 0; i < 3; ++i) cudaFree(c->scratch[i]);
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return BO_OK;
+}
+extern "C" int bo_ctx_synchronize(bo_ctx c, bo_status* st) {
+  ok_st(st);
+  CU(cudaStreamSynchronize(c->stream));
+  return BO_OK;
+}
+extern "C" uint64_t bo_ctx_local_rows(bo_ctx c) { return c->n_local; }
+extern "C" uint64_t bo_ctx_ld(bo_ctx c) { return c->ld; }
+extern "C" uint64_t bo_ctx_kernel_launches(bo_ctx c) { return c->launches; }
+extern "C" uint64_t bo_ctx_allreduces(bo_ctx c) { return c->allreduces; }
+
+// ===========================================================================
+// sketch
+// ===========================================================================
+namespace bo {
+namespace host {
+uint64_t derive_seed(uint64_t base, uint64_t stream) {  // rng.hpp:12-17
+  uint64_t z = base + 0x9e3779b97f4a7c15ULL * (stream + 1);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+// host Box-Muller stream (rng.hpp:37-49) for the tiny replicated count_gauss stage
+struct HostRng {
+  std::mt19937_64 gen;
+  bool have = false;
+  double spare = 0.0;
+  explicit HostRng(uint64_t s) : gen(s) {}
+  double normal() {
+    if (have) {
+      have = false;
+      return spare;
+    }
+    const double u1 = (static_cast<double>(gen() >> 11) + 1.0) * 0x1.0p-53;
+    const double u2 = static_cast<double>(gen() >> 11) * 0x1.0p-53;
+    const double r = std::sqrt(-2.0 * std::log(u1));
+    const double a = 6.283185307179586476925286766559 * u2;
+    spare = r * std::sin(a);
+    have = true;
+    return r * std::cos(a);
+  }
+};
+
+struct Chunk {
+  uint64_t J, len;
+};
+
+// generate draws [d0, d1) (both even) of the stream seeded with mt_seed
+int gen_stream(bo_ctx ctx, uint64_t mt_seed, const std::vector<std::pair<uint64_t, uint64_t>>& segs,
+               GenArgs ga, bo_status* st) {
+  // chunking: ~2 chunks per SM over all segments, each a multiple of 312 draws
+  uint64_t total = 0;
+  for (auto& s : segs) total += s.second - s.first;
+  if (total == 0) return BO_OK;
+  const uint64_t target = std::max<uint64_t>(312 * 16, round_up(total / (2 * (uint64_t)ctx->num_sms) + 1, 312));
+  std::vector<Chunk> chunks;
+  for (auto& s : segs)
+    for (uint64_t d = s.first; d < s.second; d += target) chunks.push_back({d, std::min(target, s.second - d)});
+  const int pw = bo::mt64::poly_words();
+  std::vector<uint64_t> polys(chunks.size() * pw), J(chunks.size()), L(chunks.size());
+  // chain x^(J0 + c*target) per segment for cache reuse
+  for (size_t c = 0; c < chunks.size(); ++c) {
+    bo::mt64::jump_poly(chunks[c].J, polys.data() + c * pw);
+    J[c] = chunks[c].J;
+    L[c] = chunks[c].len;
+  }
+  std::vector<uint64_t> pre(bo::mt64::prefix_words());
+  bo::mt64::prefix(mt_seed, pre.data());
+  uint64_t* dbuf = nullptr;
+  const size_t words = pre.size() + polys.size() + 2 * chunks.size();
+  CU(cudaMallocAsync((void**)&dbuf, words * 8, ctx->stream));
+  CU(cudaMemcpyAsync(dbuf, pre.data(), pre.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaMemcpyAsync(dbuf + pre.size(), polys.data(), polys.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaMemcpyAsync(dbuf + pre.size() + polys.size(), J.data(), J.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaMemcpyAsync(dbuf + pre.size() + polys.size() + J.size(), L.data(), L.size() * 8, cudaMemcpyHostToDevice,
+                     ctx->stream));
+  ga.prefix = dbuf;
+  ga.polys = dbuf + pre.size();
+  ga.chunk_J = dbuf + pre.size() + polys.size();
+  ga.chunk_len = ga.chunk_J + chunks.size();
+  const size_t smem = (size_t)(kPrefixWords + 8 + 2 * kMtN) * 8;
+  static bool attr = false;
+  if (!attr) {
+    CU(cudaFuncSetAttribute((const void*)sketch_gen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  sketch_gen_kernel<<<(unsigned)chunks.size(), 320, smem, ctx->stream>>>(ga);
+  CU(cudaGetLastError());
+  ctx->launches++;
+  CU(cudaFreeAsync(dbuf, ctx->stream));
+  // keep the host vectors alive until the copies are done
+  CU(cudaStreamSynchronize(ctx->stream));
+  return BO_OK;
+}
+}  // namespace host
+}  // namespace bo
+
+extern "C" int bo_sketch_build(bo_ctx ctx, int kind, uint64_t n, uint64_t shat, uint64_t seed, bo_sketch* out,
+                               bo_status* st) {
+  ok_st(st);
+  *out = nullptr;
+  if (n != ctx->n_global) return set_st(st, BO_INVALID, 0, 0.0, "sketch ambient dimension != ctx global rows");
+  const uint64_t cols = shat + 1;
+  bo_sketch s = new bo_sketch_s();
+  s->ctx = ctx;
+  s->kind = kind;
+  s->n = n;
+  uint64_t check = 0;
+  switch (kind) {
+    case BO_SKETCH_GAUSSIAN:
+      s->mhat = 2 * cols;
+      check = s->mhat;
+      break;
+    case BO_SKETCH_COUNT:
+      s->mhat = 2 * cols * cols;
+      s->mc = s->mhat;
+      check = s->mhat;
+      break;
+    case BO_SKETCH_COUNT_GAUSS:
+      s->mhat = 2 * cols;
+      s->mc = 2 * cols * cols;
+      check = s->mc;
+      break;
+    default:
+      delete s;
+      return set_st(st, BO_INVALID, 0, 0.0, "unknown sketch kind");
+  }
+  if (n <= check) {  // errors.hpp:45-49
+    delete s;
+    return set_st(st, BO_AMBIENT_TOO_SMALL, 0, 0.0, "ambient dimension n=%llu must exceed sketch size mhat=%llu",
+                  (unsigned long long)n, (unsigned long long)check);
+  }
+  if (!bo::mt64::ready()) {
+    delete s;
+    return set_st(st, BO_INVALID, 0, 0.0, "MT19937-64 jump-ahead initialisation failed");
+  }
+  const uint64_t mt_seed = derive_seed(seed, 0);  // sketch.cpp:72
+  GenArgs ga{};
+  ga.n_global = n;
+  ga.row_begin = ctx->row_begin;
+  ga.row_end = ctx->row_end;
+  const uint64_t nl = ctx->n_local;
+  std::vector<std::pair<uint64_t, uint64_t>> segs;
+  if (kind == BO_SKETCH_GAUSSIAN) {
+    s->ldth = ctx->ld;
+    cudaError_t e = cudaMalloc(&s->theta, std::max<uint64_t>(s->ldth * s->mhat, 1) * 8);
+    if (e != cudaSuccess) {
+      delete s;
+      return set_st(st, BO_CUDA, 0, 0.0, "cudaMalloc(theta) failed: %s", cudaGetErrorString(e));
+    }
+    cudaMemsetAsync(s->theta, 0, s->ldth * s->mhat * 8, ctx->stream);
+    ga.kind = 0;
+    ga.mhat = (int)s->mhat;
+    ga.scale = 1.0 / std::sqrt(double(s->mhat));
+    ga.theta = s->theta;
+    ga.ldth = s->ldth;
+    // column j needs normals [j n + a, j n + b) ; pairs start at even draws
+    if (ctx->row_begin == 0 && ctx->row_end == n) {
+      segs.push_back({0, round_up(n * s->mhat, 2)});
+    } else {
+      for (uint64_t j = 0; j < s->mhat; ++j) {
+        const uint64_t lo = (j * n + ctx->row_begin) & ~1ULL;
+        const uint64_t hi = round_up(j * n + ctx->row_end, 2);
+        if (hi > lo) segs.push_back({lo, hi});
+      }
+    }
+  } else {
+    cudaError_t e = cudaMalloc(&s->code, round_up(std::max<uint64_t>(nl, 1), 32) * 4);
+    if (e != cudaSuccess) {
+      delete s;
+      return set_st(st, BO_CUDA, 0, 0.0, "cudaMalloc(code) failed: %s", cudaGetErrorString(e));
+    }
+    cudaMemsetAsync(s->code, 0, round_up(std::max<uint64_t>(nl, 1), 32) * 4, ctx->stream);
+    ga.kind = 1;
+    ga.width = s->mc;
+    ga.code = s->code;
+    segs.push_back({2 * ctx->row_begin, 2 * ctx->row_end});
+  }
+  int rc = gen_stream(ctx, mt_seed, segs, ga, st);
+  if (rc != BO_OK) {
+    bo_sketch_destroy(s);
+    return rc;
+  }
+  if (kind == BO_SKETCH_COUNT_GAUSS) {
+    // dense stage mc x mhat from derive_seed(seed, 1) (sketch.cpp:91-95), replicated
+    HostRng rg(derive_seed(seed, 1));
+    const double scale = 1.0 / std::sqrt(double(s->mhat));
+    s->theta_g_host.resize(s->mc * s->mhat);
+    for (uint64_t j = 0; j < s->mhat; ++j)
+      for (uint64_t i = 0; i < s->mc; ++i) s->theta_g_host[i + j * s->mc] = scale * rg.normal();
+    cudaError_t e = cudaMalloc(&s->theta_g, s->theta_g_host.size() * 8);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(s->theta_g, s->theta_g_host.data(), s->theta_g_host.size() * 8, cudaMemcpyHostToDevice,
+                          ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) {
+      bo_sketch_destroy(s);
+      return set_st(st, BO_CUDA, 0, 0.0, "count_gauss stage upload failed: %s", cudaGetErrorString(e));
+    }
+  }
+  *out = s;
+  return BO_OK;
+}
+
+extern "C" int bo_sketch_from_dense(bo_ctx ctx, const double* theta, uint64_t ld, uint64_t mhat, bo_sketch* out,
+                                    bo_status* st) {
+  ok_st(st);
+  bo_sketch s = new bo_sketch_s();
+  s->ctx = ctx;
+  s->kind = BO_SKETCH_GAUSSIAN;
+  s->n = ctx->n_global;
+  s->mhat = mhat;
+  s->ldth = ctx->ld;
+  CU(cudaMalloc(&s->theta, std::max<uint64_t>(s->ldth * mhat, 1) * 8));
+  CU(cudaMemset(s->theta, 0, s->ldth * mhat * 8));
+  CU(cudaMemcpy2DAsync(s->theta, s->ldth * 8, theta, ld * 8, ctx->n_local * 8, mhat, cudaMemcpyDeviceToDevice,
+                       ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  *out = s;
+  return BO_OK;
+}
+
+extern "C" int bo_sketch_destroy(bo_sketch s) {
+  if (!s) return BO_OK;
+  cudaStreamSynchronize(s->ctx->stream);
+  if (s->own_theta) cudaFree(s->theta);
+  cudaFree(s->code);
+  cudaFree(s->theta_g);
+  delete s;
+  return BO_OK;
+}
+extern "C" uint64_t bo_sketch_size(bo_sketch s) { return s->mhat; }
+extern "C" uint64_t bo_sketch_count_width(bo_sketch s) { return s->mc; }
+extern "C" int bo_sketch_kind(bo_sketch s) { return s->kind; }
+
+extern "C" int bo_sketch_dense_to_host(bo_sketch s, double* out, bo_status* st) {
+  ok_st(st);
+  if (!s->theta) return set_st(st, BO_INVALID, 0, 0.0, "sketch has no dense row stage");
+  const uint64_t nl = s->ctx->n_local;
+  CU(cudaMemcpy2D(out, nl * 8, s->theta, s->ldth * 8, nl * 8, s->mhat, cudaMemcpyDeviceToHost));
+  return BO_OK;
+}
+extern "C" int bo_sketch_count_to_host(bo_sketch s, uint32_t* buckets, double* signs, bo_status* st) {
+  ok_st(st);
+  if (!s->code) return set_st(st, BO_INVALID, 0, 0.0, "sketch has no count stage");
+  const uint64_t nl = s->ctx->n_local;
+  std::vector<uint32_t> c(nl);
+  CU(cudaMemcpy(c.data(), s->code, nl * 4, cudaMemcpyDeviceToHost));
+  for (uint64_t i = 0; i < nl; ++i) {
+    if (buckets) buckets[i] = c[i] & 0x7fffffffu;
+    if (signs) signs[i] = (c[i] & 0x80000000u) ? -1.0 : 1.0;
+  }
+  return BO_OK;
+}
+extern "C" int bo_sketch_gauss_stage_to_host(bo_sketch s, double* out, bo_status* st) {
+  ok_st(st);
+  if (s->theta_g_host.empty()) return set_st(st, BO_INVALID, 0, 0.0, "sketch has no count_gauss stage");
+  std::memcpy(out, s->theta_g_host.data(), s->theta_g_host.size() * 8);
+  return BO_OK;
+}
+
+namespace bo {
+namespace host {
+int sketch_pass(bo_sketch sk, const double* v, uint64_t ldv, int K, int pass_id, int extra_ops, bo_status* st) {
+  bo_ctx ctx = sk->ctx;
+  PassReq r{};
+  r.kind = sk->kind == BO_SKETCH_GAUSSIAN ? PK_SKG : PK_SKC;
+  r.K = K;
+  r.V = v;
+  r.ldv = ldv;
+  r.sk = sk;
+  r.pass_id = pass_id;
+  r.fin.ops = FIN_COPY_S | extra_ops;
+  r.fin.Sout = T_(ctx, OFF_S);
+  r.fin.Rhh = T_(ctx, OFF_R1);
+  return run_pass(ctx, r, st);
+}
+}  // namespace host
+}  // namespace bo
+
+extern "C" int bo_sketch_apply(bo_sketch sk, const double* v, uint64_t ldv, uint64_t k, double* out,
+                               uint64_t ledger[4], bo_status* st) {
+  ok_st(st);
+  bo_ctx ctx = sk->ctx;
+  CU(cudaSetDevice(ctx->device));
+  const double* vv;
+  uint64_t lv;
+  TRY(stage_input(ctx, v, ldv, k, 0, &vv, &lv, st));
+  TRY(reset_status(ctx, st));
+  TRY(sketch_pass(sk, vv, lv, (int)k, 1, 0, st));
+  TRY(fetch(ctx, true, st));
+  const double* S = ctx->tiny_host + OFF_S;
+  std::memcpy(out, S, sk->mhat * k * 8);
+  if (ledger) ledger[BO_LEDGER_SKETCH]++;
+  return BO_OK;
+}
+
+// ===========================================================================
+// dense / intra-orth
+// ===========================================================================
+namespace bo {
+namespace host {
+void copy_factor_host(const double* src16, int K, double* dst /* K x K */) {
+  for (int j = 0; j < K; ++j)
+    for (int i = 0; i < K; ++i) dst[i + j * K] = src16[i + j * 16];
+}
+
+// cholqr on device: G -> R (slot Rslot) -> store Q (when q != nullptr)
+int dev_cholqr(bo_ctx ctx, const double* v, uint64_t ldv, int K, double* q, uint64_t ldq, int Rslot, int pass_id,
+               bo_status* st) {
+  PassReq g{};
+  g.kind = PK_GRAM;
+  g.K = K;
+  g.V = v;
+  g.ldv = ldv;
+  g.pass_id = pass_id;
+  g.fin.ops = FIN_CHOL;
+  g.fin.Rchol = T_(ctx, Rslot);
+  TRY(run_pass(ctx, g, st));
+  if (q) {
+    PassReq w{};
+    w.kind = PK_P1_ST;
+    w.K = K;
+    w.V = v;
+    w.ldv = ldv;
+    w.out = q;
+    w.ldo = ldq;
+    w.Rpre0 = T_(ctx, Rslot);
+    w.pass_id = pass_id + 1;
+    TRY(run_pass(ctx, w, st));
+  }
+  return BO_OK;
+}
+
+// intra-block factorization of V (n x K) per IntraKind, writing Q to q:
+// cholqr2: gram->R1, trsm(R1)+gram->R2 (Rin = R2 R1), trsm(R1,R2)->store
+// rand   : sketch->Rs(R1), trsm(R1)+gram->Rc(R2) (Rin = Rc Rs), trsm(R1,R2)->store
+// pass ids 1, 2 (+3 store); Rin in OFF_RIN
+int dev_intra(bo_ctx ctx, const double* v, uint64_t ldv, int K, int intra, bo_sketch sk, double* q, uint64_t ldq,
+              bo_status* st) {
+  if (intra == BO_INTRA_CHOLQR2) {
+    PassReq g{};
+    g.kind = PK_GRAM;
+    g.K = K;
+    g.V = v;
+    g.ldv = ldv;
+    g.pass_id = 1;
+    g.fin.ops = FIN_CHOL;
+    g.fin.Rchol = T_(ctx, OFF_R1);
+    TRY(run_pass(ctx, g, st));
+  } else {
+    TRY(sketch_pass(sk, v, ldv, K, 1, FIN_HH, st));
+  }
+  PassReq g2{};
+  g2.kind = PK_P1_GRAM;
+  g2.K = K;
+  g2.V = v;
+  g2.ldv = ldv;
+  g2.Rpre0 = T_(ctx, OFF_R1);
+  g2.pass_id = 2;
+  g2.fin.ops = FIN_CHOL | FIN_MULT;
+  g2.fin.Rchol = T_(ctx, OFF_R2);
+  g2.fin.Rin = T_(ctx, OFF_R1);
+  g2.fin.rjj = T_(ctx, OFF_RIN);
+  TRY(run_pass(ctx, g2, st));
+  if (q) {
+    PassReq w{};
+    w.kind = PK_P2_ST;
+    w.K = K;
+    w.V = v;
+    w.ldv = ldv;
+    w.out = q;
+    w.ldo = ldq;
+    w.Rpre0 = T_(ctx, OFF_R1);
+    w.Rpre1 = T_(ctx, OFF_R2);
+    w.pass_id = 3;
+    TRY(run_pass(ctx, w, st));
+  }
+  return BO_OK;
+}
+
+int write_out(bo_ctx ctx, double* q, uint64_t ldq, int K, double** target, uint64_t* ldt) {
+  if (out_ok(ctx, q, ldq)) {
+    *target = q;
+    *ldt = ldq;
+  } else {
+    *target = ctx->scratch[2];
+    *ldt = ctx->ld;
+  }
+  return BO_OK;
+}
+int finish_out(bo_ctx ctx, double* q, uint64_t ldq, int K, double* target, bo_status* st) {
+  if (target != q)
+    CU(cudaMemcpy2DAsync(q, ldq * 8, target, ctx->ld * 8, ctx->n_local * 8, K, cudaMemcpyDeviceToDevice,
+                         ctx->stream));
+  return BO_OK;
+}
+}  // namespace host
+}  // namespace bo
+
+extern "C" int bo_gram(bo_ctx ctx, const double* v, uint64_t ldv, uint64_t k, double* g, uint64_t ledger[4],
+                       bo_status* st) {
+  ok_st(st);
+  CU(cudaSetDevice(ctx->device));
+  const double* vv;
+  uint64_t lv;
+  TRY(stage_input(ctx, v, ldv, k, 0, &vv, &lv, st));
+  TRY(reset_status(ctx, st));
+  PassReq r{};
+  r.kind = PK_GRAM;
+  r.K = (int)k;
+  r.V = vv;
+  r.ldv = lv;
+  r.fin.ops = FIN_COPY_G;
+  r.fin.Gout = T_(ctx, OFF_G);
+  TRY(run_pass(ctx, r, st));
+  TRY(fetch(ctx, true, st));
+  copy_factor_host(ctx->tiny_host + OFF_G, (int)k, g);
+  if (ledger) ledger[BO_LEDGER_GRAM]++;
+  return BO_OK;
+}
+
+extern "C" int bo_apply_inv_upper(bo_ctx ctx, const double* v, uint64_t ldv, uint64_t k, const double* r, double* x,
+                                  uint64_t ldx, bo_status* st) {
+  ok_st(st);
+  CU(cudaSetDevice(ctx->device));
+  for (uint64_t j = 0; j < k; ++j)
+    if (r[j + j * k] == 0.0)
+      return set_st(st, BO_SINGULAR_TRIANGULAR, (long long)j, 0.0,
+                    "triangular factor is singular: zero diagonal at index %llu", (unsigned long long)j);
+  const double* vv;
+  uint64_t lv;
+  TRY(stage_input(ctx, v, ldv, k, 0, &vv, &lv, st));
+  double* h = ctx->tiny_host + OFF_R4;
+  for (int e = 0; e < 256; ++e) h[e] = 0.0;
+  for (uint64_t j = 0; j < k; ++j)
+    for (uint64_t i = 0; i <= j; ++i) h[i + j * 16] = r[i + j * k];
+  CU(cudaMemcpyAsync(T_(ctx, OFF_R4), h, 256 * 8, cudaMemcpyHostToDevice, ctx->stream));
+  TRY(reset_status(ctx, st));
+  double* tgt;
+  uint64_t ldt;
+  write_out(ctx, x, ldx, (int)k, &tgt, &ldt);
+  PassReq w{};
+  w.kind = PK_P1_ST;
+  w.K = (int)k;
+  w.V = vv;
+  w.ldv = lv;
+  w.out = tgt;
+  w.ldo = ldt;
+  w.Rpre0 = T_(ctx, OFF_R4);
+  TRY(run_pass(ctx, w, st));
+  TRY(finish_out(ctx, x, ldx, (int)k, tgt, st));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return BO_OK;
+}
+
+extern "C" int bo_cholqr(bo_ctx ctx, const double* v, uint64_t ldv, uint64_t k, double* q, uint64_t ldq, double* r,
+                         uint64_t ledger[4], bo_status* st) {
+  ok_st(st);
+  CU(cudaSetDevice(ctx->device));
+  const double* vv;
+  uint64_t lv;
+  TRY(stage_input(ctx, v, ldv, k, 0, &vv, &lv, st));
+  TRY(reset_status(ctx, st));
+  double* tgt;
+  uint64_t ldt;
+  write_out(ctx, q, ldq, (int)k, &tgt, &ldt);
+  TRY(dev_cholqr(ctx, vv, lv, (int)k, tgt, ldt, OFF_R1, 1, st));
+  TRY(fetch(ctx, true, st));
+  if (ledger) ledger[BO_LEDGER_GRAM]++;
+  TRY(dev_error(ctx, "cholqr", st));
+  TRY(finish_out(ctx, q, ldq, (int)k, tgt, st));
+  CU(cudaStreamSynchronize(ctx->stream));
+  if (r) copy_factor_host(ctx->tiny_host + OFF_R1, (int)k, r);
+  return BO_OK;
+}
+
+namespace bo {
+namespace host {
+int intra_api(bo_ctx ctx, const double* v, uint64_t ldv, uint64_t k, int intra, bo_sketch sk, double* q,
+              uint64_t ldq, double* r, uint64_t ledger[4], bo_status* st) {
+  ok_st(st);
+  CU(cudaSetDevice(ctx->device));
+  if (intra == BO_INTRA_RAND_CHOLQR && !sk)
+    return set_st(st, BO_INVALID, 0, 0.0, "rand_cholqr intra-orthogonalization needs a sketch operator");
+  const double* vv;
+  uint64_t lv;
+  TRY(stage_input(ctx, v, ldv, k, 0, &vv, &lv, st));
+  TRY(reset_status(ctx, st));
+  double* tgt;
+  uint64_t ldt;
+  write_out(ctx, q, ldq, (int)k, &tgt, &ldt);
+  TRY(dev_intra(ctx, vv, lv, (int)k, intra, sk, tgt, ldt, st));
+  TRY(fetch(ctx, true, st));
+  const DevStatus& d = *ctx->status_host;
+  if (ledger) {
+    // cholqr2: gram, gram ; rand_cholqr: sketch, gram (intra_orth.cpp:21-39)
+    const int upto = d.code ? d.pass : 2;
+    if (upto >= 1) ledger[intra == BO_INTRA_CHOLQR2 ? BO_LEDGER_GRAM : BO_LEDGER_SKETCH]++;
+    if (upto >= 2) ledger[BO_LEDGER_GRAM]++;
+  }
+  TRY(dev_error(ctx, "cholqr", st));
+  TRY(finish_out(ctx, q, ldq, (int)k, tgt, st));
+  CU(cudaStreamSynchronize(ctx->stream));
+  if (r) copy_factor_host(ctx->tiny_host + OFF_RIN, (int)k, r);
+  return BO_OK;
+}
+}  // namespace host
+}  // namespace bo
+
+extern "C" int bo_cholqr2(bo_ctx ctx, const double* v, uint64_t ldv, uint64_t k, double* q, uint64_t ldq, double* r,
+                          uint64_t ledger[4], bo_status* st) {
+  return intra_api(ctx, v, ldv, k, BO_INTRA_CHOLQR2, nullptr, q, ldq, r, ledger, st);
+}
+extern "C" int bo_rand_cholqr(bo_ctx ctx, const double* v, uint64_t ldv, uint64_t k, bo_sketch sk, double* q,
+                              uint64_t ldq, double* r, uint64_t ledger[4], bo_status* st) {
+  return intra_api(ctx, v, ldv, k, BO_INTRA_RAND_CHOLQR, sk, q, ldq, r, ledger, st);
+}
+
+// ===========================================================================
+// BasisStore
+// ===========================================================================
+extern "C" int bo_basis_create(bo_ctx ctx, uint64_t capacity, bo_basis* out, bo_status* st) {
+  ok_st(st);
+  *out = nullptr;
+  CU(cudaSetDevice(ctx->device));
+  bo_basis b = new bo_basis_s();
+  b->ctx = ctx;
+  b->cap = capacity;
+  cudaError_t e = cudaMalloc(&b->q, std::max<uint64_t>(ctx->ld * capacity, 1) * 8);
+  if (e != cudaSuccess) {
+    delete b;
+    return set_st(st, BO_CUDA, 0, 0.0, "cudaMalloc(basis) failed: %s", cudaGetErrorString(e));
+  }
+  cudaMemsetAsync(b->q, 0, ctx->ld * capacity * 8, ctx->stream);
+  b->r.assign(capacity * capacity, 0.0);
+  b->c.assign(capacity * capacity, 0.0);
+  b->seeded.assign(capacity, 0);
+  *out = b;
+  return BO_OK;
+}
+extern "C" int bo_basis_destroy(bo_basis b) {
+  if (!b) return BO_OK;
+  cudaStreamSynchronize(b->ctx->stream);
+  cudaFree(b->q);
+  delete b;
+  return BO_OK;
+}
+extern "C" int bo_basis_reset(bo_basis b) {
+  b->cols = 0;
+  std::fill(b->r.begin(), b->r.end(), 0.0);
+  std::fill(b->c.begin(), b->c.end(), 0.0);
+  std::fill(b->seeded.begin(), b->seeded.end(), 0);
+  b->bounds.clear();
+  b->bp_lo = 0;
+  b->sk.clear();
+  b->sk_rows = b->sk_cols = 0;
+  for (auto& l : b->ledger) l = 0;
+  return BO_OK;
+}
+extern "C" uint64_t bo_basis_cols(bo_basis b) { return b->cols; }
+extern "C" uint64_t bo_basis_capacity(bo_basis b) { return b->cap; }
+extern "C" double* bo_basis_q_device(bo_basis b, uint64_t* ld) {
+  if (ld) *ld = b->ctx->ld;
+  return b->q;
+}
+extern "C" int bo_basis_ledger(bo_basis b, uint64_t out[4]) {
+  std::memcpy(out, b->ledger, sizeof b->ledger);
+  return BO_OK;
+}
+extern "C" int bo_basis_r_copy(bo_basis b, double* out) {  // block_orth.cpp:33-38
+  for (uint64_t j = 0; j < b->cols; ++j)
+    for (uint64_t i = 0; i < b->cols; ++i) out[i + j * b->cols] = i <= j ? b->r[i + j * b->cap] : 0.0;
+  return BO_OK;
+}
+extern "C" double bo_basis_r_entry(bo_basis b, uint64_t i, uint64_t j) { return b->r[i + j * b->cap]; }
+extern "C" int bo_basis_c_copy(bo_basis b, double* out) {
+  for (uint64_t j = 0; j < b->cols; ++j)
+    for (uint64_t i = 0; i < b->cols; ++i) out[i + j * b->cols] = b->c[i + j * b->cap];
+  return BO_OK;
+}
+extern "C" int bo_basis_mark_seed(bo_basis b, uint64_t col) {  // block_orth.cpp:40-45
+  if (col >= b->cols) return BO_INVALID;
+  for (uint64_t i = 0; i < b->cap; ++i) b->c[i + col * b->cap] = 0.0;
+  b->c[col + col * b->cap] = 1.0;
+  b->seeded[col] = 1;
+  return BO_OK;
+}
+extern "C" int bo_basis_is_seed(bo_basis b, uint64_t col) { return col < b->cap && b->seeded[col]; }
+extern "C" int bo_basis_input_coeff_col(bo_basis b, uint64_t k, uint64_t len, double* out) {  // :47-52
+  const std::vector<double>& src = bo_basis_is_seed(b, k) ? b->c : b->r;
+  for (uint64_t i = 0; i < len; ++i) out[i] = src[i + k * b->cap];
+  return BO_OK;
+}
+extern "C" int bo_basis_begin_big_panel(bo_basis b, uint64_t sketch_rows, int overlap) {  // :54-57
+  b->bp_lo = b->cols - ((overlap && b->cols > 0) ? 1 : 0);
+  b->sk.clear();
+  b->sk_rows = sketch_rows;
+  b->sk_cols = 0;
+  return BO_OK;
+}
+extern "C" uint64_t bo_basis_big_panel_lo(bo_basis b) { return b->bp_lo; }
+extern "C" uint64_t bo_basis_num_boundaries(bo_basis b) { return b->bounds.size(); }
+extern "C" int bo_basis_boundaries(bo_basis b, uint64_t* out) {
+  for (size_t i = 0; i < b->bounds.size(); ++i) out[i] = b->bounds[i];
+  return BO_OK;
+}
+extern "C" uint64_t bo_basis_sketched(bo_basis b, double* out, uint64_t* rows) {
+  if (rows) *rows = b->sk_rows;
+  if (out && !b->sk.empty()) std::memcpy(out, b->sk.data(), b->sk.size() * 8);
+  return b->sk_cols;
+}
+extern "C" int bo_basis_cols_to_host(bo_basis b, uint64_t lo, uint64_t hi, double* out, bo_status* st) {
+  ok_st(st);
+  bo_ctx ctx = b->ctx;
+  if (hi < lo || hi > b->cap) return set_st(st, BO_INVALID, 0, 0.0, "bad column range");
+  CU(cudaStreamSynchronize(ctx->stream));
+  if (hi > lo)
+    CU(cudaMemcpy2D(out, ctx->n_local * 8, b->q + lo * ctx->ld, ctx->ld * 8, ctx->n_local * 8, hi - lo,
+                    cudaMemcpyDeviceToHost));
+  return BO_OK;
+}
+
+namespace bo {
+namespace host {
+// push_panel bookkeeping (block_orth.cpp:57-98) — Q columns are already in the slab
+// proj: base x k (ld ldp), diag: k x k (ld ldd)
+void push_panel_host(bo_basis b, uint64_t k, const double* proj, uint64_t ldp, const double* diag, uint64_t ldd,
+                     bool overlap) {
+  const uint64_t cap = b->cap;
+  const uint64_t base = overlap ? b->cols - 1 : b->cols;
+  if (overlap) {  // fold_overlap_column (block_orth.cpp:59-73)
+    const uint64_t k0 = b->cols - 1;
+    const double scale = diag[0];
+    const double r_diag = b->r[k0 + k0 * cap];
+    for (uint64_t i = 0; i < k0; ++i) b->r[i + k0 * cap] += r_diag * proj[i];
+    b->r[k0 + k0 * cap] = r_diag * scale;
+    if (b->seeded[k0]) {
+      const double c_diag = b->c[k0 + k0 * cap];
+      for (uint64_t i = 0; i < k0; ++i) b->c[i + k0 * cap] += c_diag * proj[i];
+      b->c[k0 + k0 * cap] = c_diag * scale;
+    }
+  }
+  for (uint64_t j = 0; j < k; ++j) {
+    const uint64_t g = base + j;
+    if (!(overlap && j == 0)) {
+      for (uint64_t i = 0; i < base; ++i) b->r[i + g * cap] = proj[i + j * ldp];
+      for (uint64_t i = 0; i <= j; ++i) b->r[base + i + g * cap] = diag[i + j * ldd];
+    }
+  }
+  b->bounds.push_back(base);
+  b->cols = base + k;
+}
+}  // namespace host
+}  // namespace bo
+
+// ===========================================================================
+// bcgs_project_range / bcgs2
+// ===========================================================================
+namespace bo {
+namespace host {
+// P1: C = Q^T V (slot Cslot) ; P2: Vhat = V - Q C (stored)
+int dev_project(bo_basis b, const double* v, uint64_t ldv, int K, uint64_t lo, uint64_t hi, double* vhat,
+                uint64_t ldvh, int Cslot, int pass_id, bo_status* st) {
+  bo_ctx ctx = b->ctx;
+  const int p = (int)(hi - lo);
+  PassReq r1{};
+  r1.kind = PK_QTX;
+  r1.K = K;
+  r1.V = v;
+  r1.ldv = ldv;
+  r1.Q = b->q + lo * ctx->ld;
+  r1.ldq = ctx->ld;
+  r1.p = p;
+  r1.pass_id = pass_id;
+  r1.fin.ops = FIN_COPY_Q;
+  r1.fin.Cq = T_(ctx, Cslot);
+  TRY(run_pass(ctx, r1, st));
+  PassReq r2{};
+  r2.kind = PK_UPD_ST;
+  r2.K = K;
+  r2.V = v;
+  r2.ldv = ldv;
+  r2.Q = r1.Q;
+  r2.ldq = ctx->ld;
+  r2.p = p;
+  r2.Cm = T_(ctx, Cslot);
+  r2.out = vhat;
+  r2.ldo = ldvh;
+  r2.pass_id = pass_id;
+  return run_pass(ctx, r2, st);
+}
+}  // namespace host
+}  // namespace bo
+
+extern "C" int bo_bcgs_project_range(bo_basis b, const double* v, uint64_t ldv, uint64_t k, uint64_t lo, uint64_t hi,
+                                     double* vhat, uint64_t ldvh, double* coeffs, bo_status* st) {
+  ok_st(st);
+  bo_ctx ctx = b->ctx;
+  CU(cudaSetDevice(ctx->device));
+  if (lo > hi || hi > b->cols) return set_st(st, BO_INVALID, 0, 0.0, "bad projection range");
+  const double* vv;
+  uint64_t lv;
+  TRY(stage_input(ctx, v, ldv, k, 0, &vv, &lv, st));
+  double* tgt;
+  uint64_t ldt;
+  write_out(ctx, vhat, ldvh, (int)k, &tgt, &ldt);
+  if (hi == lo) {  // no reduce: vhat = v
+    CU(cudaMemcpy2DAsync(vhat, ldvh * 8, vv, lv * 8, ctx->n_local * 8, k, cudaMemcpyDeviceToDevice, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return BO_OK;
+  }
+  TRY(reset_status(ctx, st));
+  TRY(dev_project(b, vv, lv, (int)k, lo, hi, tgt, ldt, OFF_C1, 1, st));
+  TRY(finish_out(ctx, vhat, ldvh, (int)k, tgt, st));
+  TRY(fetch(ctx, true, st));
+  b->ledger[BO_LEDGER_PROJECTION]++;
+  const uint64_t p = hi - lo;
+  if (coeffs)
+    for (uint64_t j = 0; j < k; ++j)
+      for (uint64_t i = 0; i < p; ++i) coeffs[i + j * p] = ctx->tiny_host[OFF_C1 + i + j * LDC];
+  return BO_OK;
+}
+
+extern "C" int bo_bcgs2(bo_basis b, const double* v, uint64_t ldv, uint64_t k, int intra, bo_sketch theta,
+                        int overlap, bo_status* st) {
+  ok_st(st);
+  bo_ctx ctx = b->ctx;
+  CU(cudaSetDevice(ctx->device));
+  const int K = (int)k;
+  const bool eff_overlap = overlap && b->cols > 0;
+  const uint64_t hi = b->cols - (eff_overlap ? 1 : 0);
+  const uint64_t base = hi;  // push_panel base == hi in both cases
+  if (base + k > b->cap) return set_st(st, BO_INVALID, 0, 0.0, "basis capacity exceeded");
+  if (intra == BO_INTRA_RAND_CHOLQR && !theta)
+    return set_st(st, BO_INVALID, 0, 0.0, "rand_cholqr intra-orthogonalization needs a sketch operator");
+  if (intra != BO_INTRA_CHOLQR2 && intra != BO_INTRA_RAND_CHOLQR)
+    return set_st(st, BO_INVALID, 0, 0.0, "unknown intra kind");
+  const double* vv;
+  uint64_t lv;
+  TRY(stage_input(ctx, v, ldv, k, 0, &vv, &lv, st));
+  double* qout = b->q + base * ctx->ld;
+  TRY(reset_status(ctx, st));
+  const bool rand = intra == BO_INTRA_RAND_CHOLQR;
+
+  if (hi == 0) {  // first panel: intra only (block_orth.cpp:212-215)
+    TRY(dev_intra(ctx, vv, lv, K, intra, theta, qout, ctx->ld, st));
+    TRY(fetch(ctx, true, st));
+    const DevStatus& d = *ctx->status_host;
+    const int upto = d.code ? d.pass : 2;
+    if (upto >= 1) b->ledger[rand ? BO_LEDGER_SKETCH : BO_LEDGER_GRAM]++;
+    if (upto >= 2) b->ledger[BO_LEDGER_GRAM]++;
+    TRY(dev_error(ctx, "cholqr", st));
+    push_panel_host(b, k, nullptr, 1, ctx->tiny_host + OFF_RIN, 16, eff_overlap);
+    return BO_OK;
+  }
+
+  const int p = (int)hi;
+  double* vhat = ctx->scratch[1];
+  const double* Q = b->q;
+  // P1: C1 = Q^T V
+  PassReq r1{};
+  r1.kind = PK_QTX;
+  r1.K = K;
+  r1.V = vv;
+  r1.ldv = lv;
+  r1.Q = Q;
+  r1.ldq = ctx->ld;
+  r1.p = p;
+  r1.pass_id = 1;
+  r1.fin.ops = FIN_COPY_Q;
+  r1.fin.Cq = T_(ctx, OFF_C1);
+  TRY(run_pass(ctx, r1, st));
+  // P2: Vhat = V - Q C1 ; G1 = Vhat^T Vhat -> R1  |  S = Theta^T Vhat -> Rs (R1)
+  PassReq r2{};
+  r2.kind = rand ? (theta->kind == BO_SKETCH_GAUSSIAN ? PK_UPD_SKG_ST : PK_UPD_SKC_ST) : PK_UPD_GRAM_ST;
+  r2.K = K;
+  r2.V = vv;
+  r2.ldv = lv;
+  r2.Q = Q;
+  r2.ldq = ctx->ld;
+  r2.p = p;
+  r2.Cm = T_(ctx, OFF_C1);
+  r2.out = vhat;
+  r2.ldo = ctx->ld;
+  r2.sk = rand ? theta : nullptr;
+  r2.pass_id = 2;
+  if (rand) {
+    r2.fin.ops = FIN_HH;
+    r2.fin.Rhh = T_(ctx, OFF_R1);
+  } else {
+    r2.fin.ops = FIN_CHOL;
+    r2.fin.Rchol = T_(ctx, OFF_R1);
+  }
+  TRY(run_pass(ctx, r2, st));
+  // P3: Y = Vhat R1^-1 ; G = Y^T Y -> R2 ; Rin = R2 R1
+  PassReq r3{};
+  r3.kind = PK_P1_GRAM;
+  r3.K = K;
+  r3.V = vhat;
+  r3.ldv = ctx->ld;
+  r3.Rpre0 = T_(ctx, OFF_R1);
+  r3.pass_id = 3;
+  r3.fin.ops = FIN_CHOL | FIN_MULT;
+  r3.fin.Rchol = T_(ctx, OFF_R2);
+  r3.fin.Rin = T_(ctx, OFF_R1);
+  r3.fin.rjj = T_(ctx, OFF_RIN);
+  TRY(run_pass(ctx, r3, st));
+  // P4: Qhat = Vhat R1^-1 R2^-1 ; C2 = Q^T Qhat
+  PassReq r4{};
+  r4.kind = PK_P2_QTX;
+  r4.K = K;
+  r4.V = vhat;
+  r4.ldv = ctx->ld;
+  r4.Q = Q;
+  r4.ldq = ctx->ld;
+  r4.p = p;
+  r4.Rpre0 = T_(ctx, OFF_R1);
+  r4.Rpre1 = T_(ctx, OFF_R2);
+  r4.pass_id = 4;
+  r4.fin.ops = FIN_COPY_Q;
+  r4.fin.Cq = T_(ctx, OFF_C2);
+  TRY(run_pass(ctx, r4, st));
+  // P5: Z = Qhat - Q C2 (in place over Vhat) ; G3 = Z^T Z -> R3 ; coeffs, rjj
+  PassReq r5{};
+  r5.kind = PK_P2_UPD_GRAM_ST;
+  r5.K = K;
+  r5.V = vhat;
+  r5.ldv = ctx->ld;
+  r5.Q = Q;
+  r5.ldq = ctx->ld;
+  r5.p = p;
+  r5.Rpre0 = T_(ctx, OFF_R1);
+  r5.Rpre1 = T_(ctx, OFF_R2);
+  r5.Cm = T_(ctx, OFF_C2);
+  r5.out = vhat;
+  r5.ldo = ctx->ld;
+  r5.pass_id = 5;
+  r5.fin.ops = FIN_CHOL | FIN_COEFF;
+  r5.fin.Rchol = T_(ctx, OFF_R3);
+  r5.fin.C1 = T_(ctx, OFF_C1);
+  r5.fin.C2 = T_(ctx, OFF_C2);
+  r5.fin.Rin = T_(ctx, OFF_RIN);
+  r5.fin.coeffs = T_(ctx, OFF_COEF);
+  r5.fin.rjj = T_(ctx, OFF_RJJ);
+  TRY(run_pass(ctx, r5, st));
+  // P6: Q_out = Z R3^-1 written in place into the basis slab
+  PassReq r6{};
+  r6.kind = PK_P1_ST;
+  r6.K = K;
+  r6.V = vhat;
+  r6.ldv = ctx->ld;
+  r6.Rpre0 = T_(ctx, OFF_R3);
+  r6.out = qout;
+  r6.ldo = ctx->ld;
+  r6.pass_id = 6;
+  TRY(run_pass(ctx, r6, st));
+
+  TRY(fetch(ctx, true, st));
+  const DevStatus& d = *ctx->status_host;
+  // ledger (block_orth.cpp:218-221): proj, intra(2), proj, gram
+  const int upto = d.code ? d.pass : 5;
+  if (upto >= 1) b->ledger[BO_LEDGER_PROJECTION]++;
+  if (upto >= 2) b->ledger[rand ? BO_LEDGER_SKETCH : BO_LEDGER_GRAM]++;
+  if (upto >= 3) b->ledger[BO_LEDGER_GRAM]++;
+  if (upto >= 4) b->ledger[BO_LEDGER_PROJECTION]++;
+  if (upto >= 5) b->ledger[BO_LEDGER_GRAM]++;
+  TRY(dev_error(ctx, "cholqr", st));
+  push_panel_host(b, k, ctx->tiny_host + OFF_COEF, LDC, ctx->tiny_host + OFF_RJJ, 16, eff_overlap);
+  return BO_OK;
+}
+
+extern "C" int bo_mt64_jump_window(uint64_t seed, uint64_t J, uint64_t* out312) {
+  if (!bo::mt64::ready()) return BO_INVALID;
+  bo::mt64::jump_window_host(seed, J, out312);
+  return BO_OK;
+}

@@ -1,0 +1,104 @@
+// bo_common.cuh — shared device-side types for the block-orthogonalization
+// kernels (status word, tiny-factor workspace layout, pass descriptors).
+#pragma once
+#include <cstdint>
+
+namespace bo {
+
+constexpr int kMaxK = 16;        // panel width bound of the streaming passes (s <= 15)
+constexpr int kRld = 16;         // leading dimension of every K x K factor in the workspace
+constexpr int kMaxPTile = 64;    // max projection columns per streaming pass
+constexpr int kConsumerWarps = 8;
+constexpr int kThreads = (kConsumerWarps + 1) * 32;  // + 1 producer warp
+
+// device status word (mirrors the reference exception set, errors.hpp:12-92)
+struct DevStatus {
+  int code;        // bo_code
+  int pass;        // which pass raised it (for ledger reconstruction)
+  long long step;  // 1-based Cholesky step / zero-diagonal index
+  double pivot;
+};
+
+enum StatusCode : int {
+  ST_OK = 0,
+  ST_CHOLESKY = 1,
+  ST_SINGULAR = 2,
+};
+
+// sketch payload kinds staged by the streaming passes
+enum SketchStage : int { SK_NONE = 0, SK_GAUSS = 1, SK_COUNT = 2 };
+
+// finalize micro-ops (bit mask), executed by one CTA after the cross-CTA /
+// cross-rank reduction of a pass
+enum FinOp : int {
+  FIN_COPY_Q = 1 << 0,     // QTX block -> Cq (ld ldcq)
+  FIN_CHOL = 1 << 1,       // GRAM block -> cholesky -> Rchol  (fails: ST_CHOLESKY)
+  FIN_HH = 1 << 2,         // SK block (or Theta_g^T SK) -> Householder R -> Rhh (fails: ST_SINGULAR)
+  FIN_PIP = 1 << 3,        // G = GRAM - QTX^T QTX before FIN_CHOL; QTX -> Cq
+  FIN_COEFF = 1 << 4,      // coeffs = C1 + C2 * Rin ; rjj = Rchol * Rin   (bcgs2 push data)
+  FIN_MULT = 1 << 5,       // rjj = Rchol * Rin (first panel)
+  FIN_COPY_G = 1 << 6,     // GRAM block -> Gout (16 x 16)
+  FIN_COPY_S = 1 << 7,     // SK block (after Theta_g) -> Sout (mh x K, ld mh)
+  FIN_CHECK_DIAG = 1 << 8  // zero diagonal of Rin_check -> ST_SINGULAR
+};
+
+struct FinArgs {
+  int ops;
+  int K, p, mh, mc;        // panel width, QTX rows, sketch rows, count width (count-gauss)
+  int pass_id;
+  double pivot_tol;
+  const double* sums;      // reduced partials
+  int off_q, ld_q;         // QTX block offset / ld inside sums
+  int off_g;               // GRAM block offset (16 x 16)
+  int off_s, ld_s;         // SK block offset / ld inside sums
+  const double* theta_g;   // count-gauss dense stage, mc x mh (ld mc)
+  double* Cq;              // FIN_COPY_Q / FIN_PIP destination
+  int ldcq;
+  double* Rchol;           // FIN_CHOL output (16 x 16)
+  double* Rhh;             // FIN_HH output
+  const double* C1;        // FIN_COEFF inputs
+  const double* C2;
+  int ldc;
+  const double* Rin;       // inner R (16 x 16)
+  double* coeffs;          // FIN_COEFF outputs (ld ldc)
+  double* rjj;
+  double* Gout;
+  double* Sout;
+  const double* Rcheck;
+  DevStatus* status;
+};
+
+// one streaming pass over the local rows
+struct PassArgs {
+  long long nrows;
+  int ntiles;
+  int K;
+  const double* V;
+  long long ldv;
+  const double* Q;
+  long long ldq;
+  int p;
+  const double* Th;        // gaussian sketch rows (local rows x mh)
+  long long ldth;
+  const uint32_t* code;    // count sketch: bucket | sign bit (local rows)
+  int mh;                  // sketch rows (gauss) / buckets (count)
+  double* out;
+  long long ldo;
+  const double* Rpre0;     // first pre-TRSM factor (16 x 16)
+  const double* Rpre1;     // second pre-TRSM factor
+  const double* Rpost;     // post-update TRSM factor
+  const double* Cm;        // update coefficients p x K (ld ldc)
+  int ldc;
+  double* partials;        // [grid][part_len]
+  double* sums;            // [part_len]
+  unsigned* counter;
+  int part_len, off_q, ld_q, off_g, off_s, ld_s;
+  int nstages;
+  int region0_dbl;         // doubles of shared region 0 (stage ring / reduction / finalize scratch)
+  int dm_len;              // tensor-core partial length (excludes the count block)
+  int fused_finalize;      // 1: last CTA runs FinArgs
+  DevStatus* status;
+  FinArgs fin;
+};
+
+}  // namespace bo

@@ -1,0 +1,168 @@
+// bo_internal.h — host-side objects behind the C ABI handles.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/bo_cuda.h"
+#include "bo_common.cuh"
+
+struct bo_ctx_s {
+  int device = 0;
+  int rank = 0, world = 1;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  void* nccl = nullptr;  // ncclComm_t
+  uint64_t n_global = 0, row_begin = 0, row_end = 0, n_local = 0, ld = 0;
+  int num_sms = 0;
+  size_t smem_optin = 0;
+  // device workspace
+  double* partials = nullptr;
+  size_t partials_cap = 0;  // doubles
+  double* sums = nullptr;
+  size_t sums_cap = 0;
+  unsigned* counter = nullptr;
+  bo::DevStatus* status = nullptr;      // device
+  bo::DevStatus* status_host = nullptr; // pinned
+  double* tiny = nullptr;               // tiny-factor workspace (device)
+  size_t tiny_cap = 0;
+  double* tiny_host = nullptr;          // pinned mirror
+  double* scratch[3] = {nullptr, nullptr, nullptr};  // ld x 16 tall scratch
+  uint64_t launches = 0;
+  uint64_t allreduces = 0;
+};
+
+struct bo_sketch_s {
+  bo_ctx ctx = nullptr;
+  int kind = 0;
+  uint64_t n = 0, mhat = 0, mc = 0;  // mc: count width (count / count_gauss)
+  double* theta = nullptr;            // gaussian local rows (ld x mhat)
+  uint64_t ldth = 0;
+  bool own_theta = true;
+  uint32_t* code = nullptr;           // count codes (local rows)
+  double* theta_g = nullptr;          // count_gauss dense stage (device, mc x mhat)
+  std::vector<double> theta_g_host;
+};
+
+struct bo_basis_s {
+  bo_ctx ctx = nullptr;
+  uint64_t cap = 0, cols = 0;
+  double* q = nullptr;  // device slab ld x cap
+  std::vector<double> r, c;  // host cap x cap
+  std::vector<char> seeded;
+  std::vector<uint64_t> bounds;
+  uint64_t bp_lo = 0;
+  std::vector<double> sk;  // sketched history sk_rows x sk_cols
+  uint64_t sk_rows = 0, sk_cols = 0;
+  uint64_t ledger[4] = {0, 0, 0, 0};
+};
+
+struct bo_op_s {
+  bo_ctx ctx = nullptr;
+  int kind = 0;  // 0 csr, 1 laplace
+  int dims = 0;
+  uint64_t k = 0;
+  uint64_t ncols = 0;
+  int* row_ptr = nullptr;  // local CSR (int32 offsets / int32 local-or-global cols)
+  int* col = nullptr;
+  double* val = nullptr;
+  uint64_t nnz = 0;
+  double a_fro = 0.0;      // ||A||_F (global)
+  // halo (world > 1): rows needed below/above the shard
+  uint64_t halo_lo = 0, halo_hi = 0;
+  double* xext = nullptr;  // extended x: [halo_lo | local | halo_hi]
+};
+
+namespace bo {
+namespace host {
+
+//           name              NPRE UPD  NPOST QTX  GRAM  SK        STORE
+#define BO_PASS_KINDS(X)                                               \
+  X(QTX, 0, false, 0, true, false, SK_NONE, false)                     \
+  X(QTX_GRAM, 0, false, 0, true, true, SK_NONE, false)                 \
+  X(GRAM, 0, false, 0, false, true, SK_NONE, false)                    \
+  X(SKG, 0, false, 0, false, false, SK_GAUSS, false)                   \
+  X(SKC, 0, false, 0, false, false, SK_COUNT, false)                   \
+  X(UPD_ST, 0, true, 0, false, false, SK_NONE, true)                   \
+  X(UPD_GRAM_ST, 0, true, 0, false, true, SK_NONE, true)               \
+  X(UPD_SKG_ST, 0, true, 0, false, false, SK_GAUSS, true)              \
+  X(UPD_SKC_ST, 0, true, 0, false, false, SK_COUNT, true)              \
+  X(P1_GRAM, 1, false, 0, false, true, SK_NONE, false)                 \
+  X(P2_QTX, 2, false, 0, true, false, SK_NONE, false)                  \
+  X(P2_UPD_GRAM_ST, 2, true, 0, false, true, SK_NONE, true)            \
+  X(P1_ST, 1, false, 0, false, false, SK_NONE, true)                   \
+  X(P2_ST, 2, false, 0, false, false, SK_NONE, true)                    \
+  X(UPD_POST_ST, 0, true, 1, false, false, SK_NONE, true)
+
+enum PassKind {
+#define X(nm, a, b, c, d, e, f, g) PK_##nm,
+  BO_PASS_KINDS(X)
+#undef X
+      PK_COUNT
+};
+struct KindInfo {
+  int npre;
+  bool upd;
+  int npost;
+  bool qtx, gram;
+  int sk;
+  bool store;
+};
+inline const KindInfo kKindInfo[PK_COUNT] = {
+#define X(nm, a, b, c, d, e, f, g) {a, b, c, d, e, f, g},
+    BO_PASS_KINDS(X)
+#undef X
+};
+
+struct PassReq {
+  int kind;
+  int K;
+  const double* V;
+  uint64_t ldv;
+  const double* Q = nullptr;
+  uint64_t ldq = 0;
+  int p = 0;
+  bo_sketch sk = nullptr;
+  double* out = nullptr;
+  uint64_t ldo = 0;
+  const double* Rpre0 = nullptr;
+  const double* Rpre1 = nullptr;
+  const double* Rpost = nullptr;
+  const double* Cm = nullptr;
+  FinArgs fin{};
+  int pass_id = 0;
+};
+
+
+// tiny workspace layout (doubles) — all K x K factors have ld 16
+constexpr int OFF_R1 = 0, OFF_R2 = 256, OFF_R3 = 512, OFF_RIN = 768, OFF_RJJ = 1024,
+              OFF_G = 1280, OFF_R4 = 1536, OFF_C1 = 2048, OFF_C2 = 3072, OFF_COEF = 4096,
+              OFF_S = 5120, TINY_LEN = 5120 + 8192;
+constexpr int LDC = 64;
+
+int set_st(bo_status* st, int code, long long index, double pivot, const char* fmt, ...);
+void ok_st(bo_status* st);
+int run_pass(bo_ctx ctx, PassReq& r, bo_status* st);
+inline double* T_(bo_ctx ctx, int off) { return ctx->tiny + off; }
+int reset_status(bo_ctx ctx, bo_status* st);
+int fetch(bo_ctx ctx, bool tiny, bo_status* st);
+int stage_input(bo_ctx ctx, const double* v, uint64_t ldv, uint64_t k, int slot, const double** out,
+                uint64_t* ldout, bo_status* st);
+bool out_ok(bo_ctx ctx, const double* q, uint64_t ldq);
+int dev_error(bo_ctx ctx, const char* chol_ctx, bo_status* st);
+int dev_intra(bo_ctx ctx, const double* v, uint64_t ldv, int K, int intra, bo_sketch sk, double* q, uint64_t ldq,
+              bo_status* st);
+int dev_cholqr(bo_ctx ctx, const double* v, uint64_t ldv, int K, double* q, uint64_t ldq, int Rslot, int pass_id,
+               bo_status* st);
+int dev_project(bo_basis b, const double* v, uint64_t ldv, int K, uint64_t lo, uint64_t hi, double* vhat,
+                uint64_t ldvh, int Cslot, int pass_id, bo_status* st);
+int sketch_pass(bo_sketch sk, const double* v, uint64_t ldv, int K, int pass_id, int extra_ops, bo_status* st);
+void push_panel_host(bo_basis b, uint64_t k, const double* proj, uint64_t ldp, const double* diag, uint64_t ldd,
+                     bool overlap);
+uint64_t derive_seed(uint64_t base, uint64_t stream);
+inline uint64_t round_up(uint64_t x, uint64_t m) { return (x + m - 1) / m * m; }
+
+}  // namespace host
+}  // namespace bo

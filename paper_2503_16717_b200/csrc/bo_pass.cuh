@@ -1,0 +1,523 @@
+// bo_pass.cuh — the streaming pass engine.
+//
+// One persistent CTA per SM walks tiles of T local rows.  A producer warp
+// stages every column segment the pass needs (panel V, projection range of
+// the basis Q, Gaussian sketch rows, Count sketch codes) into a ring of
+// shared-memory stages with bulk async copies (TMA engine) tracked by
+// mbarriers.  Eight consumer warps then, per tile:
+//   A  row-parallel triangular solves  X = V R_a^{-1} R_b^{-1}   (NPRE)
+//   U  tensor-core update              X = X - Q C               (UPD, DMMA)
+//   A' row-parallel triangular solve   X = X R^{-1}              (NPOST)
+//   S  bulk async store of X to HBM                              (STORE)
+//   R  tensor-core contractions Q^T X, X^T X, Theta^T X (DMMA) and the
+//      deterministic Count-sketch scatter (QTX, GRAM, SK)
+// Partial sums are reduced across warps, then across CTAs in fixed order by
+// the last CTA to finish, which also runs the tiny factorization of the pass
+// (bo_tiny.cuh) on one GPU.  Every HBM byte of the pass is read exactly once.
+//
+// Reference operations fused here (proj/src/dense.cpp): transpose_times :28,
+// subtract_product :60, gram :10, apply_inv_upper :166, plus the sketch
+// application proj/src/sketch.cpp:110-126.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "bo_common.cuh"
+#include "bo_ptx.cuh"
+#include "bo_tiny.cuh"
+
+namespace bo {
+
+template <int T>
+struct TileGeom {
+  static constexpr int S = T + 4;  // padded column stride (doubles): conflict-free DMMA fragments
+};
+
+// ---------------------------------------------------------------------------
+// finalize (one CTA): the tiny factorizations after a reduction
+// ---------------------------------------------------------------------------
+__device__ void finalize_dev(const FinArgs& f, double* smem_scratch /* >= 16*16*2 + 256*32 */) {
+  const int tid = threadIdx.x, nth = blockDim.x;
+  __shared__ int s_code;
+  if (tid == 0) s_code = f.status->code;
+  __syncthreads();
+  if (s_code != ST_OK) return;
+  const double* sums = f.sums;
+  double* G = smem_scratch;             // 16 x 16
+  double* sb = smem_scratch + 256;      // 16 x 16 scratch
+  double* A = smem_scratch + 512;       // sketch block for Householder
+  const int K = f.K;
+
+  if (f.ops & FIN_COPY_Q) {
+    for (int e = tid; e < f.p * K; e += nth) {
+      const int i = e % f.p, j = e / f.p;
+      f.Cq[i + j * f.ldcq] = sums[f.off_q + i + j * f.ld_q];
+    }
+  }
+  if (f.ops & FIN_COPY_G) {
+    for (int e = tid; e < 256; e += nth) f.Gout[e] = sums[f.off_g + e];
+  }
+  if (f.ops & (FIN_HH | FIN_COPY_S)) {
+    // S = sketch block (mh x K); count-gauss: S = Theta_g^T * count (sequential sums,
+    // proj/src/dense.cpp:28-42 order)
+    const int mh = f.mh;
+    for (int e = tid; e < mh * K; e += nth) {
+      const int i = e % mh, j = e / mh;
+      double v;
+      if (f.theta_g) {
+        double s = 0.0;
+        for (int r = 0; r < f.mc; ++r)
+          s = tiny::add(s, tiny::mul(f.theta_g[r + (long long)i * f.mc], sums[f.off_s + r + j * f.ld_s]));
+        v = s;
+      } else {
+        v = sums[f.off_s + i + j * f.ld_s];
+      }
+      A[i + j * mh] = v;
+      if (f.ops & FIN_COPY_S) f.Sout[i + j * mh] = v;
+    }
+    __syncthreads();
+    if (f.ops & FIN_HH) {
+      tiny::householder_r(A, mh, mh, K, f.Rhh, sb);
+      __syncthreads();
+      if (tid == 0) {
+        for (int j = 0; j < K; ++j)
+          if (f.Rhh[j + j * kRld] == 0.0) {  // apply_inv_upper throws SingularTriangular(j)
+            f.status->code = ST_SINGULAR;
+            f.status->pass = f.pass_id;
+            f.status->step = j;
+            f.status->pivot = 0.0;
+            break;
+          }
+      }
+      __syncthreads();
+      if (f.status->code != ST_OK) return;
+    }
+  }
+  if (f.ops & FIN_CHECK_DIAG) {
+    if (tid == 0) {
+      for (int j = 0; j < K; ++j)
+        if (f.Rcheck[j + j * kRld] == 0.0) {
+          f.status->code = ST_SINGULAR;
+          f.status->pass = f.pass_id;
+          f.status->step = j;
+          f.status->pivot = 0.0;
+          break;
+        }
+    }
+    __syncthreads();
+    if (f.status->code != ST_OK) return;
+  }
+  if (f.ops & FIN_CHOL) {
+    // G = GRAM block (optionally minus proj^T proj for BCGS-PIP, block_orth.cpp:245-251)
+    for (int e = tid; e < 256; e += nth) {
+      const int i = e % 16, j = e / 16;
+      double g = sums[f.off_g + e];
+      if ((f.ops & FIN_PIP) && i < K && j < K) {
+        double s = 0.0;
+        for (int l = 0; l < f.p; ++l)
+          s = tiny::add(s, tiny::mul(sums[f.off_q + l + i * f.ld_q], sums[f.off_q + l + j * f.ld_q]));
+        g = tiny::sub(g, s);
+      }
+      G[e] = g;
+    }
+    if (f.ops & FIN_PIP) {
+      for (int e = tid; e < f.p * K; e += nth) {
+        const int i = e % f.p, j = e / f.p;
+        f.Cq[i + j * f.ldcq] = sums[f.off_q + i + j * f.ld_q];
+      }
+    }
+    __syncthreads();
+    __shared__ int s_fail;
+    __shared__ double s_piv;
+    tiny::cholesky(G, K, f.pivot_tol, f.Rchol, sb, &s_fail, &s_piv);
+    if (s_fail) {
+      if (tid == 0) {
+        f.status->code = ST_CHOLESKY;
+        f.status->pass = f.pass_id;
+        f.status->step = s_fail;
+        f.status->pivot = s_piv;
+      }
+      __syncthreads();
+      return;
+    }
+  }
+  if (f.ops & FIN_COEFF) {
+    tiny::update_projection(f.C1, f.C2, f.ldc, f.p, K, f.Rin, f.coeffs);
+  }
+  if (f.ops & (FIN_COEFF | FIN_MULT)) {
+    tiny::multiply_upper(f.Rchol, f.Rin, K, f.rjj);
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) finalize_kernel(FinArgs f) {
+  __shared__ double scratch[512 + 4096];
+  finalize_dev(f, scratch);
+}
+
+// ---------------------------------------------------------------------------
+// the pass kernel
+// ---------------------------------------------------------------------------
+template <int NT, int T, int NPRE, bool UPD, int NPOST, bool QTX, bool GRAM, int SK, bool STORE>
+__global__ void __launch_bounds__(kThreads, 1) pass_kernel(const PassArgs a) {
+  constexpr int S = TileGeom<T>::S;
+  constexpr int NW = kConsumerWarps;
+  constexpr int NC = NW * 32;
+  constexpr bool XT = (NPRE > 0) || UPD || (NPOST > 0);  // X lives in the X tile
+  constexpr int MQT = kMaxPTile / 8;                     // QTX M-tiles (<= 64 columns)
+  constexpr int MST = 4;                                 // gaussian sketch M-tiles (<= 32 rows)
+  static_assert(!(QTX && UPD), "a pass either projects or updates");
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int K = a.K, p = a.p, mh = a.mh;
+  const long long nrows = a.nrows;
+
+  // stage layout: [V: K cols][Q: p cols][Th: mh cols (gauss)][code: 1 col of T u32 (count)]
+  const int ncolV = K, ncolQ = (QTX || UPD) ? p : 0, ncolT = (SK == SK_GAUSS) ? mh : 0;
+  const int stage_dbl = (ncolV + ncolQ + ncolT) * S + ((SK == SK_COUNT) ? (T / 2 + 2) : 0);
+  const int NS = a.nstages;
+  double* stages = reinterpret_cast<double*>(smem_raw);
+  double* xtile = stages + a.region0_dbl;                         // [2][K][S]
+  double* rfac = xtile + (XT ? 2 * K * S : 0);                    // [3][256]
+  double* cacc = rfac + 3 * 256;                                  // count acc [mh][K]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(cacc + ((SK == SK_COUNT) ? mh * K : 0));
+  uint64_t* full = bars;
+  uint64_t* empty = bars + NS;
+  __shared__ int s_skip;
+
+  if (tid == 0) {
+    s_skip = a.status->code != ST_OK;
+    for (int s = 0; s < NS; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], NW);
+    }
+    ptx::fence_mbar_init();
+  }
+  // factors into smem
+  if (NPRE > 0)
+    for (int e = tid; e < 256; e += blockDim.x) rfac[e] = a.Rpre0[e];
+  if (NPRE > 1)
+    for (int e = tid; e < 256; e += blockDim.x) rfac[256 + e] = a.Rpre1[e];
+  if (NPOST > 0)
+    for (int e = tid; e < 256; e += blockDim.x) rfac[512 + e] = a.Rpost[e];
+  if (SK == SK_COUNT)
+    for (int e = tid; e < mh * K; e += blockDim.x) cacc[e] = 0.0;
+  __syncthreads();
+  if (s_skip) return;  // an earlier pass broke down: this one is a no-op
+
+  const int ntiles = a.ntiles;
+  const int my_tiles = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+
+  // ------------------------------------------------------------ producer
+  if (warp == NW) {
+    for (int it = 0; it < my_tiles; ++it) {
+      const int s = it % NS;
+      const long long row0 = (long long)(blockIdx.x + (long long)it * gridDim.x) * T;
+      const long long valid = nrows - row0 < T ? nrows - row0 : T;
+      const uint32_t vb = (uint32_t)(((valid + 3) & ~3LL) * 8);  // 32-byte multiple
+      const uint32_t cb = (uint32_t)(((valid + 3) & ~3LL) * 4);
+      ptx::mbar_wait(&empty[s], ((it / NS) & 1) ^ 1);
+      double* st = stages + (size_t)s * stage_dbl;
+      if (lane == 0) {
+        const uint32_t total = vb * (ncolV + ncolQ + ncolT) + ((SK == SK_COUNT) ? cb : 0);
+        ptx::mbar_arrive_expect_tx(&full[s], total);
+      }
+      __syncwarp();
+      for (int c = lane; c < ncolV; c += 32) ptx::bulk_g2s(st + c * S, a.V + c * a.ldv + row0, vb, &full[s]);
+      for (int c = lane; c < ncolQ; c += 32)
+        ptx::bulk_g2s(st + (ncolV + c) * S, a.Q + c * a.ldq + row0, vb, &full[s]);
+      for (int c = lane; c < ncolT; c += 32)
+        ptx::bulk_g2s(st + (ncolV + ncolQ + c) * S, a.Th + c * a.ldth + row0, vb, &full[s]);
+      if (SK == SK_COUNT && lane == 0)
+        ptx::bulk_g2s(st + (ncolV + ncolQ) * S, a.code + row0, cb, &full[s]);
+    }
+  } else {
+    // ---------------------------------------------------------- consumers
+    // update coefficients as DMMA B fragments:  B[kk][j] = -C[c0+kk][nj*8+j]
+    double cfr[UPD ? MQT * 2 : 1][NT];
+    if (UPD) {
+#pragma unroll
+      for (int ks = 0; ks < MQT * 2; ++ks)
+#pragma unroll
+        for (int nj = 0; nj < NT; ++nj) {
+          const int r = ks * 4 + t4, c = nj * 8 + g;
+          cfr[ks][nj] = (r < p && c < K) ? -a.Cm[r + c * a.ldc] : 0.0;
+        }
+    }
+    double accq[QTX ? MQT : 1][NT][2];
+    double accg[GRAM ? NT : 1][NT][2];
+    double accs[(SK == SK_GAUSS) ? MST : 1][NT][2];
+#pragma unroll
+    for (int i = 0; i < (QTX ? MQT : 1); ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j) accq[i][j][0] = accq[i][j][1] = 0.0;
+#pragma unroll
+    for (int i = 0; i < (GRAM ? NT : 1); ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j) accg[i][j][0] = accg[i][j][1] = 0.0;
+#pragma unroll
+    for (int i = 0; i < ((SK == SK_GAUSS) ? MST : 1); ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j) accs[i][j][0] = accs[i][j][1] = 0.0;
+
+    for (int it = 0; it < my_tiles; ++it) {
+      const int s = it % NS;
+      const long long row0 = (long long)(blockIdx.x + (long long)it * gridDim.x) * T;
+      const int valid = (int)(nrows - row0 < T ? nrows - row0 : T);
+      double* st = stages + (size_t)s * stage_dbl;
+      const double* stV = st;
+      const double* stQ = st + ncolV * S;
+      const double* stT = st + (ncolV + ncolQ) * S;
+      const uint32_t* stC = reinterpret_cast<const uint32_t*>(st + (ncolV + ncolQ) * S);
+      double* xt = xtile + (it & 1) * K * S;
+
+      if (STORE && tid < K) ptx::bulk_wait_read0();  // previous tile's store drained its X buffer
+      ptx::mbar_wait(&full[s], (it / NS) & 1);
+
+      // ---- A: pre-TRSM, thread per row
+      if (NPRE > 0) {
+        if (tid < T) {
+          const int r = tid;
+          double x[kMaxK];
+#pragma unroll
+          for (int c = 0; c < kMaxK; ++c) x[c] = (c < K && r < valid) ? stV[c * S + r] : 0.0;
+#pragma unroll
+          for (int f = 0; f < NPRE; ++f) {
+            const double* R = rfac + f * 256;
+#pragma unroll
+            for (int j = 0; j < kMaxK; ++j) {
+              if (j < K) {
+#pragma unroll
+                for (int i = 0; i < j; ++i) {
+                  const double rij = R[i + j * kRld];
+                  if (rij != 0.0) x[j] = tiny::sub(x[j], tiny::mul(rij, x[i]));
+                }
+                x[j] = tiny::div(x[j], R[j + j * kRld]);
+              }
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < kMaxK; ++c)
+            if (c < K) xt[c * S + r] = (r < valid) ? x[c] : 0.0;
+        }
+        ptx::named_bar_sync(1, NC);
+      }
+
+      // ---- U: X = X0 - Q C on tensor cores, one 8-row group per warp step
+      if (UPD) {
+        const double* x0 = (NPRE > 0) ? xt : stV;
+        for (int rg = warp; rg < T / 8; rg += NW) {
+          const int r = rg * 8 + g;
+          const bool rv = r < valid;
+          double d[NT][2];
+#pragma unroll
+          for (int nj = 0; nj < NT; ++nj)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int c = nj * 8 + 2 * t4 + e;
+              d[nj][e] = (rv && c < K) ? x0[c * S + r] : 0.0;
+            }
+#pragma unroll
+          for (int ks = 0; ks < MQT * 2; ++ks) {
+            if (ks * 4 < p) {
+              const int c = ks * 4 + t4;
+              const double av = (rv && c < p) ? stQ[c * S + r] : 0.0;
+#pragma unroll
+              for (int nj = 0; nj < NT; ++nj) ptx::dmma(d[nj][0], d[nj][1], av, cfr[ks][nj]);
+            }
+          }
+#pragma unroll
+          for (int nj = 0; nj < NT; ++nj)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int c = nj * 8 + 2 * t4 + e;
+              if (c < K) xt[c * S + r] = rv ? d[nj][e] : 0.0;
+            }
+        }
+        ptx::named_bar_sync(1, NC);
+      }
+
+      // ---- A': post-TRSM
+      if (NPOST > 0) {
+        if (tid < T) {
+          const int r = tid;
+          double x[kMaxK];
+#pragma unroll
+          for (int c = 0; c < kMaxK; ++c) x[c] = (c < K) ? xt[c * S + r] : 0.0;
+          const double* R = rfac + 512;
+#pragma unroll
+          for (int j = 0; j < kMaxK; ++j) {
+            if (j < K) {
+#pragma unroll
+              for (int i = 0; i < j; ++i) {
+                const double rij = R[i + j * kRld];
+                if (rij != 0.0) x[j] = tiny::sub(x[j], tiny::mul(rij, x[i]));
+              }
+              x[j] = tiny::div(x[j], R[j + j * kRld]);
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < kMaxK; ++c)
+            if (c < K) xt[c * S + r] = (r < valid) ? x[c] : 0.0;
+        }
+        ptx::named_bar_sync(1, NC);
+      }
+
+      const double* X = XT ? xt : stV;
+
+      // ---- S: bulk store of the X tile
+      if (STORE && tid < K) {
+        ptx::fence_proxy_async_smem();
+        ptx::bulk_s2g(a.out + (long long)tid * a.ldo + row0, xt + tid * S, (uint32_t)(valid * 8));
+        ptx::bulk_commit();
+      }
+
+      // ---- R: contractions on tensor cores, one 4-row k-step per warp step
+      if (QTX || GRAM || SK == SK_GAUSS) {
+        for (int ks = warp; ks < T / 4; ks += NW) {
+          const int r = ks * 4 + t4;
+          const bool rv = r < valid;
+          double bx[NT];
+#pragma unroll
+          for (int nj = 0; nj < NT; ++nj) {
+            const int c = nj * 8 + g;
+            bx[nj] = (rv && c < K) ? X[c * S + r] : 0.0;
+          }
+          if (QTX) {
+#pragma unroll
+            for (int mi = 0; mi < MQT; ++mi) {
+              if (mi * 8 < p) {
+                const int c = mi * 8 + g;
+                const double av = (rv && c < p) ? stQ[c * S + r] : 0.0;
+#pragma unroll
+                for (int nj = 0; nj < NT; ++nj) ptx::dmma(accq[mi][nj][0], accq[mi][nj][1], av, bx[nj]);
+              }
+            }
+          }
+          if (GRAM) {
+#pragma unroll
+            for (int mi = 0; mi < NT; ++mi)
+#pragma unroll
+              for (int nj = 0; nj < NT; ++nj)
+                if (mi <= nj) ptx::dmma(accg[mi][nj][0], accg[mi][nj][1], bx[mi], bx[nj]);
+          }
+          if (SK == SK_GAUSS) {
+#pragma unroll
+            for (int mi = 0; mi < MST; ++mi) {
+              if (mi * 8 < mh) {
+                const int c = mi * 8 + g;
+                const double av = (rv && c < mh) ? stT[c * S + r] : 0.0;
+#pragma unroll
+                for (int nj = 0; nj < NT; ++nj) ptx::dmma(accs[mi][nj][0], accs[mi][nj][1], av, bx[nj]);
+              }
+            }
+          }
+        }
+      }
+      if (SK == SK_COUNT) {
+        // deterministic scatter: warp w owns buckets b % NW == w; rows of a
+        // bucket are added in ascending row order (proj/src/sketch.cpp:54-58)
+        for (int g32 = 0; g32 < T / 32; ++g32) {
+          const int r = g32 * 32 + lane;
+          const bool rv = r < valid;
+          const uint32_t code = rv ? stC[r] : 0u;
+          const int b = (int)(code & 0x7fffffffu);
+          const bool mine = rv && (b % NW) == warp;
+          const unsigned key = mine ? (unsigned)b : (0x80000000u | (unsigned)lane);
+          const unsigned grp = __match_any_sync(0xffffffffu, key);
+          if (mine && (__ffs(grp) - 1) == lane) {
+            unsigned m = grp;
+            while (m) {
+              const int q = __ffs(m) - 1;
+              m &= m - 1;
+              const int rq = g32 * 32 + q;
+              const double sg = (stC[rq] & 0x80000000u) ? -1.0 : 1.0;
+              for (int c = 0; c < K; ++c)
+                cacc[b + c * mh] = tiny::add(cacc[b + c * mh], tiny::mul(sg, X[c * S + rq]));
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&empty[s]);
+    }
+    if (STORE && tid < K) ptx::bulk_wait0();
+
+    // ---- per-warp fragments -> shared, then fixed-order sum over warps
+    ptx::named_bar_sync(1, NC);  // all stages consumed: reuse stage memory
+    double* red = stages;        // [NW][dm_len]
+    const int dm_len = a.dm_len;
+    for (int e = lane; e < dm_len; e += 32) red[warp * dm_len + e] = 0.0;
+    __syncwarp();
+    if (QTX) {
+#pragma unroll
+      for (int mi = 0; mi < MQT; ++mi)
+#pragma unroll
+        for (int nj = 0; nj < NT; ++nj)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int i = mi * 8 + g, j = nj * 8 + 2 * t4 + e;
+            if (i < a.ld_q && j < 16) red[warp * dm_len + a.off_q + i + j * a.ld_q] = accq[mi][nj][e];
+          }
+    }
+    if (GRAM) {
+#pragma unroll
+      for (int mi = 0; mi < NT; ++mi)
+#pragma unroll
+        for (int nj = 0; nj < NT; ++nj)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int i = mi * 8 + g, j = nj * 8 + 2 * t4 + e;
+            if (mi <= nj) {
+              red[warp * dm_len + a.off_g + i + j * 16] = accg[mi][nj][e];
+              if (mi < nj) red[warp * dm_len + a.off_g + j + i * 16] = accg[mi][nj][e];
+            }
+          }
+    }
+    if (SK == SK_GAUSS) {
+#pragma unroll
+      for (int mi = 0; mi < MST; ++mi)
+#pragma unroll
+        for (int nj = 0; nj < NT; ++nj)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int i = mi * 8 + g, j = nj * 8 + 2 * t4 + e;
+            if (i < a.ld_s && j < 16) red[warp * dm_len + a.off_s + i + j * a.ld_s] = accs[mi][nj][e];
+          }
+    }
+    ptx::named_bar_sync(1, NC);
+    double* part = a.partials + (size_t)blockIdx.x * dm_len;
+    for (int e = tid; e < dm_len; e += NC) {
+      double sum = 0.0;
+      for (int w = 0; w < NW; ++w) sum += red[w * dm_len + e];
+      part[e] = sum;
+    }
+    if (SK == SK_COUNT) {
+      for (int e = tid; e < mh * K; e += NC) {
+        const int i = e % mh, j = e / mh;
+        part[a.off_s + i + j * a.ld_s] = cacc[e];
+      }
+    }
+  }
+
+  // ---- cross-CTA reduction by the last CTA (fixed CTA order: deterministic)
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = (atomicAdd(a.counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int e = tid; e < a.part_len; e += blockDim.x) {
+    double sum = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) sum += __ldcg(a.partials + (size_t)b * a.part_len + e);
+    a.sums[e] = sum;
+  }
+  if (tid == 0) *a.counter = 0u;
+  __threadfence();
+  __syncthreads();
+  if (a.fused_finalize) finalize_dev(a.fin, reinterpret_cast<double*>(smem_raw));
+}
+
+}  // namespace bo
