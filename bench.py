@@ -1,0 +1,386 @@
+#!/usr/bin/env python
+"""Benchmark: block orthogonalization (randomized BCGS2) on B200.
+
+Workload (BASELINE.json configs[1]): n = 8e6 rows, s = 10
+(k = 11 columns per panel), a sequence of six bcgs2 calls with p = 0, 11, ..,
+55 prior basis columns, RandCholQR intra-block factorization with a Gaussian
+sketch of 2(s+1) = 22 rows.  One "step" = one 6-call sequence on a fresh
+BasisStore.  Rows are sharded across ranks (strong scaling of the fixed
+8e6-row problem); the only collectives are the per-ledger-event all-reduces.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Prints ONE JSON line (rank 0).  value = algorithmic HBM GB/s of the whole job
+(8 * n * 1199 bytes per sequence) ; ms_per_step = sequence time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "BOrth time & HBM GB/s (8M rows, s=10) at 1/2/4/8 B200; GMRES time/restart"
+WORDS_PER_ROW_SEQ = None  # computed from the schedule
+
+
+def algo_words_per_row(ps, k):
+    """p=0 call 4k words/row; p>0 call 4p + 9k."""
+    return sum(4 * k if p == 0 else 4 * p + 9 * k for p in ps)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=8_000_000)
+    ap.add_argument("--s", type=int, default=10)
+    ap.add_argument("--panels", type=int, default=6)
+    ap.add_argument("--intra", default="rand_cholqr", choices=["rand_cholqr", "cholqr2"])
+    ap.add_argument("--sketch", default="gaussian", choices=["gaussian", "count", "countgauss"])
+    ap.add_argument("--kappa", type=float, default=1e2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-rows", type=int, default=1 << 18)
+    ap.add_argument("--profile-only", action="store_true", help="short run for ncu")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    def __init__(self):
+        self.samples = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        dev = os.environ.get("LOCAL_RANK", "0")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", dev, f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+
+        def rd():
+            for line in self.proc.stdout:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 8:
+                    self.samples.append(parts)
+
+        self.thread = threading.Thread(target=rd, daemon=True)
+        self.thread.start()
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for s in self.samples:
+            for nm, v in zip(names, s[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# --------------------------------------------------------------- reference --
+def cpu_reference_sequence(n, k, panels, intra, kappa, reps=1):
+    """The unmodified reference (oracle/_ref, compiled from /root/reference
+    sources) timed on one host core: same 6-call bcgs2 sequence at n rows."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    from py_oracle import Oracle, have_ref
+    which = "ref" if have_ref() else "orc"
+    o = Oracle(which)
+    v = o.gen_glued(n, panels, k, kappa, kappa, 7)
+    sk = o.sketch_build(0, n, k - 1, 1).h if intra == 1 else None
+    times = []
+    for _ in range(reps):
+        b = o.basis_new(n, panels * k)
+        t0 = time.perf_counter()
+        for p in range(panels):
+            r = o.bcgs2(b, v[:, p * k:(p + 1) * k], intra, sk)
+            assert r.code == 0, r.msg
+        times.append(time.perf_counter() - t0)
+        o.basis_free(b)
+    return which, min(times)
+
+
+def run_reference_arm(args):
+    """--impl reference: the reference CPU implementation on the host cores
+    (single-threaded by design, proj/include/blkorth/dense.hpp:121-122)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    k = args.s + 1
+    intra = 1 if args.intra == "rand_cholqr" else 0
+    ps = [p * k for p in range(args.panels)]
+    words = algo_words_per_row(ps, k)
+    n = args.cpu_rows
+    for _ in range(max(args.warmup, 0) and 1):
+        cpu_reference_sequence(n, k, args.panels, intra, args.kappa, 1)
+    tot = 0.0
+    which = "ref"
+    for _ in range(args.steps):
+        which, t = cpu_reference_sequence(n, k, args.panels, intra, args.kappa, 1)
+        tot += t
+    sec = tot / max(args.steps, 1)
+    gbs = 8.0 * n * words / sec / 1e9
+    out = {
+        "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (gen_glued, kappa=%g)" % args.kappa,
+        "config": {"workload": "C2 bcgs2 sequence (p=0..%d, k=%d) on a %d-row sample of the 8e6-row workload"
+                   % (ps[-1], k, n), "n_rows_sample": n, "s": args.s, "panels": args.panels, "intra": args.intra},
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": 1,
+                         "kind": "reference" if which == "ref" else "port",
+                         "sample": f"{n} rows x {args.panels} panels, one sequence per step"},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+# --------------------------------------------------------------------- ours --
+def make_panels(P, ctx, torch, n_global, k, panels, kappa_panel, kappa_global, seed):
+    """Synthetic glued-style panels (problems.cpp:21-61 structure): V_p = U_p
+    diag(sigma_p) W_p^T with U orthonormal (Gaussian panels orthonormalised by
+    this library's own BCGS2) and W_p random orthogonal; sigma log-spaced."""
+    total = panels * k
+    g = torch.Generator(device=ctx.device)
+    g.manual_seed(1000 + seed * 7919 + ctx.rank)
+    st = P.BasisStore(ctx, total)
+    for p in range(panels):
+        raw = torch.randn((k, ctx.ld), generator=g, device=ctx.device, dtype=torch.float64)
+        raw[:, ctx.n_local:] = 0
+        P.bcgs2(st, raw, P.borth.CHOLQR2)
+    U = st.q_device().clone()
+    st.close()
+    rs = np.random.default_rng(seed)
+    span = max(kappa_global / kappa_panel, 1.0)
+    out = []
+    for p in range(panels):
+        scale = 1.0 if panels == 1 else span ** (-p / (panels - 1))
+        sig = np.array([scale * (kappa_panel ** (-c / (k - 1)) if k > 1 else 1.0) for c in range(k)])
+        w, _ = np.linalg.qr(rs.standard_normal((k, k)))
+        M = torch.from_numpy((np.diag(sig) @ w.T)).to(ctx.device)  # V^T = M^T U_p^T
+        vp = (M.T @ U[p * k:(p + 1) * k]).contiguous()
+        out.append(vp)
+    del U
+    return out
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+    import torch
+    import torch.distributed as dist
+    import paper_2503_16717_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    n = args.n
+    k = args.s + 1
+    rb, re_ = n * rank // world, n * (rank + 1) // world
+    nid = None
+    if world > 1:
+        obj = [P.Context.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nid = obj[0]
+    ctx = P.Context(n, device=local, rank=rank, world=world, row_begin=rb, row_end=re_, nccl_id=nid)
+    intra = P.borth.RAND_CHOLQR if args.intra == "rand_cholqr" else P.borth.CHOLQR2
+    torch.cuda.set_stream(ctx.stream)  # all torch work of this script on the library stream
+    panels = make_panels(P, ctx, torch, n, k, args.panels, args.kappa, args.kappa, 7)
+    theta = P.SketchOperator.build(ctx, args.sketch, n, args.s, 1) if intra == P.borth.RAND_CHOLQR else None
+    store = P.BasisStore(ctx, args.panels * k)
+    ps = [p * k for p in range(args.panels)]
+    words = algo_words_per_row(ps, k)
+    algo_bytes = 8.0 * n * words  # whole job
+    stream = ctx.stream
+
+    def step():
+        store.reset()
+        for vp in panels:
+            P.bcgs2(store, vp, intra, theta)
+
+    for _ in range(max(args.warmup, 3) if not args.profile_only else 1):
+        step()
+    if args.profile_only:
+        step()
+        ctx.synchronize()
+        return
+
+    # ---- headline: device time of K sequences (events on the library stream)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler()
+    clk.start()
+    launches0 = ctx.kernel_launches
+    ar0 = ctx.allreduces
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1)
+    launches = ctx.kernel_launches - launches0
+    allreduces = ctx.allreduces - ar0
+    if world > 1:
+        t = torch.tensor([ms], device=ctx.device, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    ms_step = ms / args.steps
+    value = algo_bytes / (ms_step / 1e3) / 1e9
+
+    # ---- per-kernel roofline: live CUDA events around each pass launch
+    ctx.profile(True)
+    for _ in range(max(1, min(args.steps, 3))):
+        step()
+    recs = ctx.profile_read()
+    ctx.profile(False)
+    kinds = {}
+    for r in recs:
+        d = kinds.setdefault(r["kind"], {"ms": 0.0, "bytes": 0, "launches": 0})
+        d["ms"] += r["ms"]
+        d["bytes"] += r["bytes"]
+        d["launches"] += 1
+    tot_ms = sum(d["ms"] for d in kinds.values())
+    top = max(kinds.items(), key=lambda kv: kv[1]["ms"])
+    peak, peak_src = measured_peak()
+    achieved = top[1]["bytes"] / (top[1]["ms"] / 1e3) / 1e9
+    passes_all = sum(d["bytes"] for d in kinds.values()) / (tot_ms / 1e3) / 1e9
+
+    # ---- e2e: reference-facing C-ABI calls with host buffers (pinned)
+    e2e = None
+    if not args.no_e2e:
+        host_v = [torch.empty((k, ctx.n_local), dtype=torch.float64, pin_memory=True) for _ in panels]
+        for hv, vp in zip(host_v, panels):
+            hv.copy_(vp[:, : ctx.n_local])
+        dev_v = [ctx.panel(k) for _ in panels]
+        host_q = torch.empty((args.panels * k, ctx.n_local), dtype=torch.float64, pin_memory=True)
+        h2d = sum(hv.numel() * 8 for hv in host_v)
+        d2h = host_q.numel() * 8 + (args.panels * k) ** 2 * 8
+
+        def e2e_step():
+            store.reset()
+            for hv, dv in zip(host_v, dev_v):
+                dv[:, : ctx.n_local].copy_(hv, non_blocking=True)
+                P.bcgs2(store, dv, intra, theta)
+            slab = store.q_device()
+            host_q.copy_(slab[: args.panels * k, : ctx.n_local], non_blocking=True)
+            r = store.r_copy()
+            torch.cuda.current_stream().synchronize()
+            return r
+
+        e2e_step()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        nrep = max(1, min(args.steps, 3))
+        for _ in range(nrep):
+            e2e_step()
+        torch.cuda.synchronize()
+        e2e_ms = (time.perf_counter() - t0) * 1e3 / nrep
+        if world > 1:
+            t = torch.tensor([e2e_ms], device=ctx.device, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": algo_bytes / (e2e_ms / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "path": "bo_bcgs2 via ctypes; panels H2D from pinned host, basis Q and R D2H, every step"}
+        del host_v, dev_v, host_q
+
+    # ---- orthogonality check of the final basis (sanity, untimed)
+    q = store.q_device()[: args.panels * k, : ctx.n_local]
+    gq = (q @ q.T)
+    if world > 1:
+        dist.all_reduce(gq)
+    orth = float(torch.linalg.matrix_norm(torch.eye(gq.shape[0], device=gq.device, dtype=gq.dtype) - gq, ord=2))
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            which, sec = cpu_reference_sequence(args.cpu_rows, k, args.panels, intra, args.kappa, 2)
+            cpu = {"value": 8.0 * args.cpu_rows * words / sec / 1e9, "unit": "GB/s", "cores": 1,
+                   "kind": "reference" if which == "ref" else "port",
+                   "sample": f"{args.cpu_rows} rows x {args.panels} panels (one {args.intra} sequence, best of 2), "
+                             f"host core of the GPU box"}
+        except Exception as ex:  # pragma: no cover
+            cpu = {"value": None, "unit": "GB/s", "cores": 1, "kind": "reference", "sample": f"failed: {ex}"}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64",
+            "data": f"synthetic glued-style panels (kappa={args.kappa:g}), Gaussian sketch seed 1",
+            "config": {"workload": f"C2 microbench: {args.intra} BCGS2, n={n} rows, s={args.s} (k={k}), "
+                                   f"{args.panels} panels p=0..{ps[-1]}, sketch {args.sketch} mhat={2 * k}",
+                       "n_rows": n, "s": args.s, "panels": args.panels, "intra": args.intra,
+                       "parallelism": f"row-shard x{world}",
+                       "l2": "inputs (%.1f GB/step) larger than L2 (126 MB); no flush" % (8 * n * k * args.panels / 1e9),
+                       "algo_words_per_row": words},
+            "roofline": {"bound": "hbm", "kernel": top[0], "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                         "share_of_step": top[1]["ms"] / tot_ms, "all_passes_gbs": passes_all,
+                         "per_kind": {kk: {"ms_per_step": d["ms"] / max(1, min(args.steps, 3)),
+                                           "gbs": d["bytes"] / (d["ms"] / 1e3) / 1e9,
+                                           "launches_per_step": d["launches"] // max(1, min(args.steps, 3))}
+                                      for kk, d in sorted(kinds.items(), key=lambda kv: -kv[1]["ms"])}},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "allreduces": allreduces,
+            "clocks": clocks,
+            "orth_error": orth,
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -99,6 +99,18 @@ uint64_t bo_ctx_ld(bo_ctx ctx);
 uint64_t bo_ctx_kernel_launches(bo_ctx ctx);
 /* physical all-reduces issued (world > 1) */
 uint64_t bo_ctx_allreduces(bo_ctx ctx);
+/* Per-launch profiling of the streaming passes with CUDA events on the ctx
+ * stream (bench.py roofline).  enable != 0 clears and starts recording. */
+typedef struct {
+  int kind;          /* pass kind id (bo_pass_kind_name) */
+  int k, p, mh;      /* panel width, projection columns, sketch rows */
+  uint64_t rows;     /* local rows streamed */
+  uint64_t bytes;    /* HBM bytes the pass must move (reads + writes) */
+  float ms;          /* device time of the launch */
+} bo_prof_record;
+int bo_ctx_profile(bo_ctx ctx, int enable);
+int bo_ctx_profile_read(bo_ctx ctx, bo_prof_record* out, int max, int* count, bo_status* st);
+const char* bo_pass_kind_name(int kind);
 
 /* -------------------------------------------------------------- sketch -- */
 /* SketchOperator::build (sketch.hpp:28, sketch.cpp:66-99).  The Count

@@ -46,6 +46,11 @@ class SolveReport(C.Structure):
     ]
 
 
+class ProfRecord(C.Structure):
+    _fields_ = [("kind", C.c_int), ("k", C.c_int), ("p", C.c_int), ("mh", C.c_int), ("rows", u64),
+                ("bytes", u64), ("ms", C.c_float)]
+
+
 SP = C.POINTER(Status)
 
 # name: (restype, argtypes)
@@ -60,6 +65,9 @@ _SIGS = {
     "bo_ctx_ld": (u64, [vp]),
     "bo_ctx_kernel_launches": (u64, [vp]),
     "bo_ctx_allreduces": (u64, [vp]),
+    "bo_ctx_profile": (C.c_int, [vp, C.c_int]),
+    "bo_ctx_profile_read": (C.c_int, [vp, C.POINTER(ProfRecord), C.c_int, C.POINTER(C.c_int), SP]),
+    "bo_pass_kind_name": (C.c_char_p, [C.c_int]),
     "bo_sketch_build": (C.c_int, [vp, C.c_int, u64, u64, u64, C.POINTER(vp), SP]),
     "bo_sketch_from_dense": (C.c_int, [vp, vp, u64, u64, C.POINTER(vp), SP]),
     "bo_sketch_destroy": (C.c_int, [vp]),

@@ -20,6 +20,7 @@ streams only; every computation is a kernel in libbo_cuda.so.
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -165,7 +166,9 @@ class Context:
         self.row_begin, self.row_end = row_begin, row_end
         self.device = torch.device("cuda", device)
         torch.cuda.set_device(self.device)
-        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        # the library runs on this (non-default) stream; torch work that feeds
+        # it (from_host, panel) is issued on the same stream
+        self.stream = stream if stream is not None else torch.cuda.Stream(self.device)
         h = C.c_void_p()
         idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
         _call(self.lib.bo_ctx_create, device, rank, world, idbuf, n, row_begin, row_end,
@@ -173,6 +176,7 @@ class Context:
         self.h = h
         self.n_local = int(self.lib.bo_ctx_local_rows(h))
         self.ld = int(self.lib.bo_ctx_ld(h))
+        self._children = weakref.WeakSet()
 
     @staticmethod
     def nccl_unique_id() -> bytes:
@@ -185,7 +189,8 @@ class Context:
     def panel(self, k: int, zero: bool = True):
         t = self.torch
         f = t.zeros if zero else t.empty
-        return f((k, self.ld), dtype=t.float64, device=self.device)
+        with t.cuda.stream(self.stream):
+            return f((k, self.ld), dtype=t.float64, device=self.device)
 
     def from_host(self, a: np.ndarray):
         """n_local x k host array -> device panel (k, ld)."""
@@ -194,11 +199,13 @@ class Context:
             a = a[:, None]
         assert a.shape[0] == self.n_local, (a.shape, self.n_local)
         p = self.panel(a.shape[1])
-        p[:, : self.n_local] = self.torch.from_numpy(np.ascontiguousarray(a.T)).to(self.device)
+        with self.torch.cuda.stream(self.stream):
+            p[:, : self.n_local] = self.torch.from_numpy(np.ascontiguousarray(a.T)).to(self.device)
         return p
 
     def to_host(self, p, k: int | None = None) -> np.ndarray:
         k = p.shape[0] if k is None else k
+        self.stream.synchronize()
         return p[:k, : self.n_local].detach().cpu().numpy().T.copy()
 
     def synchronize(self):
@@ -212,8 +219,24 @@ class Context:
     def allreduces(self) -> int:
         return int(self.lib.bo_ctx_allreduces(self.h))
 
+    def profile(self, enable: bool = True):
+        self.lib.bo_ctx_profile(self.h, int(enable))
+
+    def profile_read(self) -> list:
+        cnt = C.c_int()
+        _call(self.lib.bo_ctx_profile_read, self.h, None, 0, C.byref(cnt))
+        buf = (L.ProfRecord * max(cnt.value, 1))()
+        _call(self.lib.bo_ctx_profile_read, self.h, buf, cnt.value, C.byref(cnt))
+        out = []
+        for r in list(buf)[: cnt.value]:
+            out.append({"kind": self.lib.bo_pass_kind_name(r.kind).decode(), "k": r.k, "p": r.p, "mh": r.mh,
+                        "rows": r.rows, "bytes": r.bytes, "ms": r.ms})
+        return out
+
     def close(self):
         if getattr(self, "h", None):
+            for ch in list(self._children):
+                ch.close()
             self.lib.bo_ctx_destroy(self.h)
             self.h = None
 
@@ -238,6 +261,7 @@ class SketchOperator:
 
     def __init__(self, ctx: Context, h):
         self.ctx, self.h = ctx, h
+        ctx._children.add(self)
 
     @classmethod
     def build(cls, ctx: Context, kind, n: int, shat: int, seed: int):
@@ -313,11 +337,13 @@ def _intra(fn_name, ctx: Context, v, ledger, theta=None, q=None):
     r = np.zeros((k, k), order="F")
     led = _ledger_in(ledger)
     fn = getattr(ctx.lib, fn_name)
-    if theta is None:
-        _call(fn, ctx.h, _ptr(v), _ld_of(v), k, _ptr(q), _ld_of(q), _dp(r), led)
-    else:
-        _call(fn, ctx.h, _ptr(v), _ld_of(v), k, theta.h, _ptr(q), _ld_of(q), _dp(r), led)
-    _ledger_out(ledger, led)
+    try:
+        if theta is None:
+            _call(fn, ctx.h, _ptr(v), _ld_of(v), k, _ptr(q), _ld_of(q), _dp(r), led)
+        else:
+            _call(fn, ctx.h, _ptr(v), _ld_of(v), k, theta.h, _ptr(q), _ld_of(q), _dp(r), led)
+    finally:  # ledger events before a breakdown stay counted
+        _ledger_out(ledger, led)
     return QrResult(q, r)
 
 
@@ -352,9 +378,11 @@ def recursive_cholqr(ctx: Context, v, ledger: ReduceLedger | None = None) -> Rec
     dn = np.zeros(k)
     nk, nd, depth = C.c_uint64(), C.c_uint64(), C.c_uint64()
     led = _ledger_in(ledger)
-    _call(ctx.lib.bo_recursive_cholqr, ctx.h, _ptr(v), _ld_of(v), k, _ptr(q), _ld_of(q), _dp(coeffs), kept,
-          C.byref(nk), disc, _dp(dn), C.byref(nd), C.byref(depth), led)
-    _ledger_out(ledger, led)
+    try:
+        _call(ctx.lib.bo_recursive_cholqr, ctx.h, _ptr(v), _ld_of(v), k, _ptr(q), _ld_of(q), _dp(coeffs), kept,
+              C.byref(nk), disc, _dp(dn), C.byref(nd), C.byref(depth), led)
+    finally:
+        _ledger_out(ledger, led)
     return RecursiveQr(q[: nk.value], coeffs[: nk.value, :].copy(), list(kept)[: nk.value],
                        list(disc)[: nd.value], list(dn[: nd.value]), depth.value)
 
@@ -386,6 +414,7 @@ class BasisStore:
         _call(ctx.lib.bo_basis_create, ctx.h, capacity, C.byref(h))
         self.h = h
         self.capacity = capacity
+        ctx._children.add(self)
 
     def close(self):
         if getattr(self, "h", None):
@@ -548,6 +577,7 @@ class Operator:
 
     def __init__(self, ctx: Context, h):
         self.ctx, self.h = ctx, h
+        ctx._children.add(self)
 
     @classmethod
     def csr(cls, ctx: Context, ncols: int, row_ptr, col, val):

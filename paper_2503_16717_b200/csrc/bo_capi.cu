@@ -253,9 +253,27 @@ int run_pass(bo_ctx ctx, PassReq& r, bo_status* st) {
       attr_set[(const void*)fn] = total;
     }
   }
+  cudaEvent_t pe0 = nullptr, pe1 = nullptr;
+  if (ctx->profiling) {
+    while (ctx->ev_pool.size() < ctx->ev_used + 2) {
+      cudaEvent_t e;
+      CU(cudaEventCreate(&e));
+      ctx->ev_pool.push_back(e);
+    }
+    pe0 = ctx->ev_pool[ctx->ev_used++];
+    pe1 = ctx->ev_pool[ctx->ev_used++];
+    CU(cudaEventRecord(pe0, ctx->stream));
+  }
   fn<<<grid, kThreads, total, ctx->stream>>>(a);
   CU(cudaGetLastError());
   ctx->launches++;
+  if (ctx->profiling) {
+    CU(cudaEventRecord(pe1, ctx->stream));
+    const int ncols = r.K + ((ki.qtx || ki.upd) ? r.p : 0) + (ki.sk == SK_GAUSS ? mh : 0);
+    const uint64_t rows = ctx->n_local;
+    const uint64_t bytes = rows * (8ull * ncols + (ki.sk == SK_COUNT ? 4ull : 0ull) + (ki.store ? 8ull * r.K : 0ull));
+    ctx->prof.push_back({r.kind, r.K, r.p, mh, rows, bytes, pe0, pe1});
+  }
   if (ctx->world > 1) {
     NcclApi& nc = nccl();
     int rc = nc.AllReduce(ctx->sums, ctx->sums, (size_t)a.part_len, kNcclFloat64, kNcclSum, ctx->nccl,
@@ -432,6 +450,35 @@ extern "C" uint64_t bo_ctx_local_rows(bo_ctx c) { return c->n_local; }
 extern "C" uint64_t bo_ctx_ld(bo_ctx c) { return c->ld; }
 extern "C" uint64_t bo_ctx_kernel_launches(bo_ctx c) { return c->launches; }
 extern "C" uint64_t bo_ctx_allreduces(bo_ctx c) { return c->allreduces; }
+extern "C" int bo_ctx_profile(bo_ctx c, int enable) {
+  c->profiling = enable;
+  if (enable) {
+    c->prof.clear();
+    c->ev_used = 0;
+  }
+  return BO_OK;
+}
+extern "C" int bo_ctx_profile_read(bo_ctx c, bo_prof_record* out, int max, int* count, bo_status* st) {
+  ok_st(st);
+  CU(cudaStreamSynchronize(c->stream));
+  int m = 0;
+  for (auto& r : c->prof) {
+    if (m >= max) break;
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, r.e0, r.e1));
+    out[m++] = {r.kind, r.K, r.p, r.mh, r.rows, r.bytes, ms};
+  }
+  if (count) *count = (int)c->prof.size();
+  return BO_OK;
+}
+extern "C" const char* bo_pass_kind_name(int kind) {
+  static const char* names[] = {
+#define X(nm, a, b, c, d, e, f, g) #nm,
+      BO_PASS_KINDS(X)
+#undef X
+  };
+  return (kind >= 0 && kind < PK_COUNT) ? names[kind] : "?";
+}
 
 // ===========================================================================
 // sketch

@@ -32,6 +32,16 @@ struct bo_ctx_s {
   double* scratch[3] = {nullptr, nullptr, nullptr};  // ld x 16 tall scratch
   uint64_t launches = 0;
   uint64_t allreduces = 0;
+  // profiling
+  struct ProfRec {
+    int kind, K, p, mh;
+    uint64_t rows, bytes;
+    cudaEvent_t e0, e1;
+  };
+  int profiling = 0;
+  std::vector<ProfRec> prof;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
 };
 
 struct bo_sketch_s {

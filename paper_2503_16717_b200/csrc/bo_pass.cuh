@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(kThreads, 1) pass_kernel(const PassArgs a) {
       // ---- S: bulk store of the X tile
       if (STORE && tid < K) {
         ptx::fence_proxy_async_smem();
-        ptx::bulk_s2g(a.out + (long long)tid * a.ldo + row0, xt + tid * S, (uint32_t)(valid * 8));
+        ptx::bulk_s2g(a.out + (long long)tid * a.ldo + row0, xt + tid * S, (uint32_t)(((valid + 1) & ~1) * 8));
         ptx::bulk_commit();
       }
 
@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(kThreads, 1) pass_kernel(const PassArgs a) {
           }
     }
     ptx::named_bar_sync(1, NC);
-    double* part = a.partials + (size_t)blockIdx.x * dm_len;
+    double* part = a.partials + (size_t)blockIdx.x * a.part_len;
     for (int e = tid; e < dm_len; e += NC) {
       double sum = 0.0;
       for (int w = 0; w < NW; ++w) sum += red[w * dm_len + e];

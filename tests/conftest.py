@@ -1,0 +1,57 @@
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "oracle"))
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) GPU")
+    config.addinivalue_line("markers", "slow: long-running")
+
+
+@pytest.fixture(scope="session")
+def orc():
+    from py_oracle import Oracle
+    return Oracle("orc")
+
+
+@pytest.fixture(scope="session")
+def ref():
+    from py_oracle import Oracle, have_ref
+    if not have_ref():
+        pytest.skip("reference build oracle/_ref unavailable (no /root/reference on this host)")
+    return Oracle("ref")
+
+
+@pytest.fixture(scope="session")
+def gpu():
+    """the CUDA extension must load and a GPU must be present (no fallback)"""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2503_16717_b200 as P
+    P._lib.load()
+    return P
+
+
+def rel_err(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    den = max(np.max(np.abs(b)), 1e-300)
+    return float(np.max(np.abs(a - b)) / den) if a.size else 0.0
+
+
+def orth_err(q):
+    q = np.asarray(q)
+    g = q.T @ q
+    return float(np.linalg.norm(np.eye(q.shape[1]) - g, 2))
+
+
+def kappa_tol(kappa, floor=1e-10):
+    """parity contract: max(1e-10, 10 kappa eps)"""
+    return max(floor, 10.0 * kappa * 2.220446049250313e-16)
