@@ -6,6 +6,8 @@
 // factorization runs on device inside the pass epilogue (bo_tiny.cuh).  The
 // host mirrors BasisStore's small R/C bookkeeping exactly as the reference
 // (proj/src/block_orth.cpp:10-153).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
@@ -117,20 +119,78 @@ constexpr int kNcclSum = 0;
 namespace bo {
 namespace host {
 
-typedef void (*PassFn)(const PassArgs);
+typedef void (*PassFn)(const PassArgs, const CUtensorMap, const CUtensorMap, const CUtensorMap);
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }();
+  return fn;
+}
+// 2-D map over `cols` columns of `rows` doubles (leading dimension ld), box = S rows x cols
+int make_tmap(CUtensorMap* m, const double* base, uint64_t rows, uint64_t cols, uint64_t ld, int S, bo_status* st) {
+  std::memset(m, 0, sizeof *m);
+  if (!base || cols == 0) return BO_OK;
+  auto fn = encode_fn();
+  if (!fn) return set_st(st, BO_CUDA, 0, 0.0, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {rows, cols};
+  const cuuint64_t strides[1] = {ld * 8};
+  const cuuint32_t box[2] = {(cuuint32_t)S, (cuuint32_t)cols};
+  const cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)base, dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_st(st, BO_CUDA, (long long)r, 0.0, "cuTensorMapEncodeTiled failed (%d): rows=%llu cols=%llu ld=%llu",
+                  (int)r, (unsigned long long)rows, (unsigned long long)cols, (unsigned long long)ld);
+  return BO_OK;
+}
 
 template <int NT, int T>
 PassFn pass_fn(int kind) {
   switch (kind) {
 #define X(nm, a, b, c, d, e, f, g) \
   case PK_##nm:                    \
-    return pass_kernel<NT, T, a, b, c, d, e, f, g>;
+    return pass_kernel<NT, T, a, b, c, d, e, f, g, false>;
     BO_PASS_KINDS(X)
 #undef X
   }
   return nullptr;
 }
-PassFn get_pass_fn(int nt, int T, int kind) {
+// triangular-solve passes specialised on the panel width (s = 5, 10, 15)
+template <int KC>
+PassFn pass_fn_kc(int kind) {
+  constexpr int NT = KC <= 8 ? 1 : 2;
+  switch (kind) {
+#define X(nm, a, b, c, d, e, f, g)                              \
+  case PK_##nm:                                                 \
+    if constexpr (a > 0 || c > 0)                               \
+      return pass_kernel<NT, 128, a, b, c, d, e, f, g, false, KC>; \
+    else                                                        \
+      return nullptr;
+    BO_PASS_KINDS(X)
+#undef X
+  }
+  return nullptr;
+}
+PassFn get_pass_fn(int nt, int T, int kind, bool exact, int K) {
+  if (exact)  // standalone apply_inv_upper: bit-exact substitution (dense.cpp:166-186)
+    return nt == 1 ? (PassFn)pass_kernel<1, 64, 1, false, 0, false, false, SK_NONE, true, true>
+                   : (PassFn)pass_kernel<2, 64, 1, false, 0, false, false, SK_NONE, true, true>;
+  const KindInfo& ki = kKindInfo[kind];
+  if (T == 128 && (ki.npre > 0 || ki.npost > 0)) {
+    PassFn f = nullptr;
+    if (K == 6) f = pass_fn_kc<6>(kind);
+    if (K == 11) f = pass_fn_kc<11>(kind);
+    if (K == 16) f = pass_fn_kc<16>(kind);
+    if (f) return f;
+  }
   if (nt == 1) return T == 128 ? pass_fn<1, 128>(kind) : pass_fn<1, 64>(kind);
   return T == 128 ? pass_fn<2, 128>(kind) : pass_fn<2, 64>(kind);
 }
@@ -179,27 +239,42 @@ int run_pass(bo_ctx ctx, PassReq& r, bo_status* st) {
 
   const int nt = r.K <= 8 ? 1 : 2;
   const size_t avail = std::min<size_t>(ctx->smem_optin, 227 * 1024) - 1024;  // static smem headroom
-  int T = 128, NS = 0;
+  // Tile choice: maximise the bytes the producer can keep in flight
+  // ((NS-1) stages, Little's law against ~1-2 us HBM latency), prefer T=128.
+  static const int tile_env = [] {
+    const char* e = getenv("BO_TILE");
+    return e ? atoi(e) : 0;
+  }();
+  int T = 0, NS = 0;
   size_t region0 = 0, total = 0;
   for (int tt : {128, 64}) {
+    if (r.exact && tt != 64) continue;
+    if (tile_env && tt != tile_env) continue;
     const int S = tt + 4;
-    const int ncol = r.K + ((ki.qtx || ki.upd) ? r.p : 0) + (ki.sk == SK_GAUSS ? mh : 0);
-    const size_t stage = ((size_t)ncol * S + (ki.sk == SK_COUNT ? (tt / 2 + 2) : 0)) * 8;
+    const StageLayout SL = stage_layout(r.K, (ki.qtx || ki.upd) ? r.p : 0, ki.sk == SK_GAUSS ? mh : 0,
+                                        ki.sk == SK_COUNT, tt);
+    const size_t stage = (size_t)SL.stage * 8;
     const bool xt = ki.npre > 0 || ki.upd || ki.npost > 0;
-    const size_t fixed = (xt ? 2 * (size_t)r.K * S * 8 : 0) + 3 * 256 * 8 +
-                         (ki.sk == SK_COUNT ? (size_t)mh * r.K * 8 : 0) + 2 * 4 * 8;
+    const size_t fixed = (xt ? 2 * (size_t)r.K * S * 8 : 0) + (3 * 256 + 48) * 8 +
+                         (ki.sk == SK_COUNT ? (size_t)mh * r.K * 8 : 0) + 2 * kMaxStages * 8;
     const size_t need_red = (size_t)kConsumerWarps * dm_len * 8;
     const size_t need_fin = (512 + (size_t)std::max(mh, 1) * 16 + 64) * 8;
-    int ns = (int)std::min<size_t>(4, (avail - fixed) / stage);
-    if (ns >= 2 || tt == 64) {
-      if (ns < 1) return set_st(st, BO_INVALID, 0, 0.0, "pass does not fit in shared memory");
+    if (avail <= fixed) continue;
+    int ns = (int)std::min<size_t>(kMaxStages, (avail - fixed) / stage);
+    if (ns < 1) continue;
+    const size_t r0 = round_up(std::max({(size_t)ns * stage, need_red, need_fin}), 128);
+    if (r0 + fixed > avail) continue;
+    // TMA moves one box per operand per tile: prefer the larger tile once two
+    // stages fit (double buffering), else the deeper ring.
+    const bool better = T == 0 || (ns >= 2 && NS < 2);
+    if (better) {
       T = tt;
       NS = ns;
-      region0 = std::max({(size_t)ns * stage, need_red, need_fin});
-      total = region0 + fixed;
-      break;
+      region0 = r0;
+      total = r0 + fixed;
     }
   }
+  if (T == 0) return set_st(st, BO_INVALID, 0, 0.0, "pass does not fit in shared memory");
   if (total > avail) return set_st(st, BO_INVALID, 0, 0.0, "pass does not fit in shared memory (%zu bytes)", total);
   a.nstages = NS;
   a.region0_dbl = (int)(region0 / 8);
@@ -242,7 +317,7 @@ int run_pass(bo_ctx ctx, PassReq& r, bo_status* st) {
   a.fin = f;
   a.fused_finalize = (ctx->world == 1) ? 1 : 0;
 
-  PassFn fn = get_pass_fn(nt, T, r.kind);
+  PassFn fn = get_pass_fn(nt, T, r.kind, r.exact, r.K);
   static std::mutex mu;
   static std::unordered_map<const void*, size_t> attr_set;
   {
@@ -264,7 +339,15 @@ int run_pass(bo_ctx ctx, PassReq& r, bo_status* st) {
     pe1 = ctx->ev_pool[ctx->ev_used++];
     CU(cudaEventRecord(pe0, ctx->stream));
   }
-  fn<<<grid, kThreads, total, ctx->stream>>>(a);
+  CUtensorMap tmV, tmQ, tmT;
+  {
+    const int S = T + 4;
+    TRY(make_tmap(&tmV, r.V, ctx->n_local, r.K, r.ldv, S, st));
+    TRY(make_tmap(&tmQ, (ki.qtx || ki.upd) ? r.Q : nullptr, ctx->n_local, r.p, r.ldq, S, st));
+    TRY(make_tmap(&tmT, ki.sk == SK_GAUSS ? r.sk->theta : nullptr, ctx->n_local, mh,
+                  ki.sk == SK_GAUSS ? r.sk->ldth : 0, S, st));
+  }
+  fn<<<grid, kThreads, total, ctx->stream>>>(a, tmV, tmQ, tmT);
   CU(cudaGetLastError());
   ctx->launches++;
   if (ctx->profiling) {
@@ -920,6 +1003,7 @@ extern "C" int bo_apply_inv_upper(bo_ctx ctx, const double* v, uint64_t ldv, uin
   w.out = tgt;
   w.ldo = ldt;
   w.Rpre0 = T_(ctx, OFF_R4);
+  w.exact = true;
   TRY(run_pass(ctx, w, st));
   TRY(finish_out(ctx, x, ldx, (int)k, tgt, st));
   CU(cudaStreamSynchronize(ctx->stream));

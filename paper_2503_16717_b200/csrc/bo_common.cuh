@@ -9,7 +9,25 @@ constexpr int kMaxK = 16;        // panel width bound of the streaming passes (s
 constexpr int kRld = 16;         // leading dimension of every K x K factor in the workspace
 constexpr int kMaxPTile = 64;    // max projection columns per streaming pass
 constexpr int kConsumerWarps = 8;
+constexpr int kMaxStages = 8;    // shared-memory stage ring depth bound
 constexpr int kThreads = (kConsumerWarps + 1) * 32;  // + 1 producer warp
+
+// Shared-memory stage layout (doubles): every operand block starts on a
+// 128-byte boundary (TMA destination alignment); column stride S = T + 4.
+struct StageLayout {
+  int offV, offQ, offT, offC, stage;
+};
+__host__ __device__ inline int ru16(int x) { return (x + 15) & ~15; }
+__host__ __device__ inline StageLayout stage_layout(int K, int ncolQ, int ncolT, bool count, int T) {
+  const int S = T + 4;
+  StageLayout L;
+  L.offV = 0;
+  L.offQ = ru16(K * S);
+  L.offT = L.offQ + ru16(ncolQ * S);
+  L.offC = L.offT + ru16(ncolT * S);
+  L.stage = L.offC + (count ? ru16(T / 2) : 0);
+  return L;
+}
 
 // device status word (mirrors the reference exception set, errors.hpp:12-92)
 struct DevStatus {

@@ -143,6 +143,7 @@ struct PassReq {
   const double* Cm = nullptr;
   FinArgs fin{};
   int pass_id = 0;
+  bool exact = false;  // bit-exact substitution (standalone apply_inv_upper only)
 };
 
 

@@ -19,6 +19,7 @@
 // subtract_product :60, gram :10, apply_inv_upper :166, plus the sketch
 // application proj/src/sketch.cpp:110-126.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "bo_common.cuh"
@@ -154,36 +155,113 @@ __global__ void __launch_bounds__(256) finalize_kernel(FinArgs f) {
   finalize_dev(f, scratch);
 }
 
+
+// X = X R^{-1} for one row held in registers (proj/src/dense.cpp:166-186).
+// Right-looking schedule: at step j, x_j is divided by r_jj and then removed
+// from every later column l.  Each x_l still receives its subtractions in
+// the reference order i = 0..l-1 before its division, so with EXACT the
+// result is bit-identical to apply_inv_upper; the (K - j) independent
+// updates per step give the ILP the left-looking loop lacks.  Without EXACT,
+// subtractions are fused (FMA) and the division is a multiply by 1/r_jj.
+template <bool EXACT, int KC>
+__device__ __forceinline__ void row_trsm(double (&x)[kMaxK], const double* R, const double* rinv, int K) {
+  constexpr int KM = KC ? KC : kMaxK;  // compile-time width when specialised
+#pragma unroll
+  for (int j = 0; j < KM; ++j) {
+    if (KC || j < K) {
+      x[j] = EXACT ? tiny::div(x[j], R[j + j * kRld]) : x[j] * rinv[j];
+#pragma unroll
+      for (int l = j + 1; l < KM; ++l) {
+        if (KC || l < K) {
+          const double rjl = R[j + l * kRld];
+          if (EXACT) {
+            if (rjl != 0.0) x[l] = tiny::sub(x[l], tiny::mul(rjl, x[j]));
+          } else {
+            x[l] = fma(-rjl, x[j], x[l]);  // branch-free: a zero coefficient is a no-op
+          }
+        }
+      }
+    }
+  }
+}
+
+
+// several independent rows per thread, interleaved for ILP
+template <bool EXACT, int KC, int NR>
+__device__ __forceinline__ void row_trsm_n(double (&x)[NR][kMaxK], const double* R, const double* rinv, int K) {
+  constexpr int KM = KC ? KC : kMaxK;
+#pragma unroll
+  for (int j = 0; j < KM; ++j) {
+    if (KC || j < K) {
+      const double dj = rinv[j];
+#pragma unroll
+      for (int q = 0; q < NR; ++q) x[q][j] = EXACT ? tiny::div(x[q][j], R[j + j * kRld]) : x[q][j] * dj;
+#pragma unroll
+      for (int l = j + 1; l < KM; ++l) {
+        if (KC || l < K) {
+          const double rjl = R[j + l * kRld];
+#pragma unroll
+          for (int q = 0; q < NR; ++q) {
+            if (EXACT) {
+              if (rjl != 0.0) x[q][l] = tiny::sub(x[q][l], tiny::mul(rjl, x[q][j]));
+            } else {
+              x[q][l] = fma(-rjl, x[q][j], x[q][l]);
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // the pass kernel
 // ---------------------------------------------------------------------------
-template <int NT, int T, int NPRE, bool UPD, int NPOST, bool QTX, bool GRAM, int SK, bool STORE>
-__global__ void __launch_bounds__(kThreads, 1) pass_kernel(const PassArgs a) {
+// Warp roles (kThreads = 9 warps):
+//   warp 8        producer: one 2-D TMA box per operand per tile (V, Q range,
+//                 Theta) + a 1-D bulk copy of the Count codes, mbarrier ring.
+//   warps 0..7    consumers.  Without a pre-TRSM they form one group that runs
+//                 U -> A' -> S -> R on each tile.  With a pre-TRSM (NPRE > 0)
+//                 they split: warps 0-3 solve rows (A) into a double-buffered
+//                 X tile while warps 4-7 run U/S/R on the previous tile, handed
+//                 over with named-barrier arrive/sync pairs.
+template <int NT, int T, int NPRE, bool UPD, int NPOST, bool QTX, bool GRAM, int SK, bool STORE, bool EXACT,
+          int KC = 0>
+__global__ void __launch_bounds__(kThreads, 1)
+    pass_kernel(const __grid_constant__ PassArgs a, const __grid_constant__ CUtensorMap tmV,
+                const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmT) {
   constexpr int S = TileGeom<T>::S;
   constexpr int NW = kConsumerWarps;
-  constexpr int NC = NW * 32;
+  constexpr bool SPLIT = NPRE > 0;
+  constexpr int GAW = SPLIT ? 2 : 0;       // row-solve warps (2 rows per thread)
+  constexpr int GW = NW - GAW;             // warps of the U/S/R group
+  constexpr int GT = GW * 32;
+  constexpr int GBAR = SPLIT ? 6 : 1;  // named barrier of the U/S/R group
   constexpr bool XT = (NPRE > 0) || UPD || (NPOST > 0);  // X lives in the X tile
-  constexpr int MQT = kMaxPTile / 8;                     // QTX M-tiles (<= 64 columns)
-  constexpr int MST = 4;                                 // gaussian sketch M-tiles (<= 32 rows)
+  constexpr int MQT = kMaxPTile / 8;
+  constexpr int MST = 4;
   static_assert(!(QTX && UPD), "a pass either projects or updates");
+  static_assert(!STORE || XT, "stores come from the X tile");
+  static_assert(!SPLIT || T <= GAW * 64, "row-solve group handles two rows per thread");
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t4 = lane & 3;
-  const int K = a.K, p = a.p, mh = a.mh;
+  const int K = KC ? KC : a.K;
+  const int p = a.p, mh = a.mh;
   const long long nrows = a.nrows;
 
-  // stage layout: [V: K cols][Q: p cols][Th: mh cols (gauss)][code: 1 col of T u32 (count)]
-  const int ncolV = K, ncolQ = (QTX || UPD) ? p : 0, ncolT = (SK == SK_GAUSS) ? mh : 0;
-  const int stage_dbl = (ncolV + ncolQ + ncolT) * S + ((SK == SK_COUNT) ? (T / 2 + 2) : 0);
+  const int ncolQ = (QTX || UPD) ? p : 0, ncolT = (SK == SK_GAUSS) ? mh : 0;
+  const StageLayout L = stage_layout(K, ncolQ, ncolT, SK == SK_COUNT, T);
   const int NS = a.nstages;
   double* stages = reinterpret_cast<double*>(smem_raw);
   double* xtile = stages + a.region0_dbl;                         // [2][K][S]
   double* rfac = xtile + (XT ? 2 * K * S : 0);                    // [3][256]
-  double* cacc = rfac + 3 * 256;                                  // count acc [mh][K]
+  double* rinv = rfac + 3 * 256;                                  // [3][16]
+  double* cacc = rinv + 48;                                       // count acc [mh][K]
   uint64_t* bars = reinterpret_cast<uint64_t*>(cacc + ((SK == SK_COUNT) ? mh * K : 0));
   uint64_t* full = bars;
-  uint64_t* empty = bars + NS;
+  uint64_t* empty = bars + kMaxStages;
   __shared__ int s_skip;
 
   if (tid == 0) {
@@ -194,7 +272,6 @@ __global__ void __launch_bounds__(kThreads, 1) pass_kernel(const PassArgs a) {
     }
     ptx::fence_mbar_init();
   }
-  // factors into smem
   if (NPRE > 0)
     for (int e = tid; e < 256; e += blockDim.x) rfac[e] = a.Rpre0[e];
   if (NPRE > 1)
@@ -204,6 +281,11 @@ __global__ void __launch_bounds__(kThreads, 1) pass_kernel(const PassArgs a) {
   if (SK == SK_COUNT)
     for (int e = tid; e < mh * K; e += blockDim.x) cacc[e] = 0.0;
   __syncthreads();
+  if (tid < 48) {
+    const int f = tid / 16, j = tid % 16;
+    rinv[tid] = 1.0 / rfac[f * 256 + j + j * kRld];
+  }
+  __syncthreads();
   if (s_skip) return;  // an earlier pass broke down: this one is a no-op
 
   const int ntiles = a.ntiles;
@@ -211,29 +293,26 @@ __global__ void __launch_bounds__(kThreads, 1) pass_kernel(const PassArgs a) {
 
   // ------------------------------------------------------------ producer
   if (warp == NW) {
-    for (int it = 0; it < my_tiles; ++it) {
-      const int s = it % NS;
-      const long long row0 = (long long)(blockIdx.x + (long long)it * gridDim.x) * T;
-      const long long valid = nrows - row0 < T ? nrows - row0 : T;
-      const uint32_t vb = (uint32_t)(((valid + 3) & ~3LL) * 8);  // 32-byte multiple
-      const uint32_t cb = (uint32_t)(((valid + 3) & ~3LL) * 4);
-      ptx::mbar_wait(&empty[s], ((it / NS) & 1) ^ 1);
-      double* st = stages + (size_t)s * stage_dbl;
-      if (lane == 0) {
-        const uint32_t total = vb * (ncolV + ncolQ + ncolT) + ((SK == SK_COUNT) ? cb : 0);
-        ptx::mbar_arrive_expect_tx(&full[s], total);
+    if (lane == 0) {
+      ptx::prefetch_tmap(&tmV);
+      if (ncolQ) ptx::prefetch_tmap(&tmQ);
+      if (ncolT) ptx::prefetch_tmap(&tmT);
+      const uint32_t box_bytes = (uint32_t)(S * 8 * (K + ncolQ + ncolT));
+      for (int it = 0; it < my_tiles; ++it) {
+        const int s = it % NS;
+        const long long row0 = (long long)(blockIdx.x + (long long)it * gridDim.x) * T;
+        const long long valid = nrows - row0 < T ? nrows - row0 : T;
+        const uint32_t cb = (SK == SK_COUNT) ? (uint32_t)(((valid + 3) & ~3LL) * 4) : 0u;
+        ptx::mbar_wait(&empty[s], ((it / NS) & 1) ^ 1);
+        double* st = stages + (size_t)s * L.stage;
+        ptx::mbar_arrive_expect_tx(&full[s], box_bytes + cb);
+        ptx::tma_load_2d(st + L.offV, &tmV, (int)row0, 0, &full[s]);
+        if (ncolQ) ptx::tma_load_2d(st + L.offQ, &tmQ, (int)row0, 0, &full[s]);
+        if (ncolT) ptx::tma_load_2d(st + L.offT, &tmT, (int)row0, 0, &full[s]);
+        if (SK == SK_COUNT) ptx::bulk_g2s(st + L.offC, a.code + row0, cb, &full[s]);
       }
-      __syncwarp();
-      for (int c = lane; c < ncolV; c += 32) ptx::bulk_g2s(st + c * S, a.V + c * a.ldv + row0, vb, &full[s]);
-      for (int c = lane; c < ncolQ; c += 32)
-        ptx::bulk_g2s(st + (ncolV + c) * S, a.Q + c * a.ldq + row0, vb, &full[s]);
-      for (int c = lane; c < ncolT; c += 32)
-        ptx::bulk_g2s(st + (ncolV + ncolQ + c) * S, a.Th + c * a.ldth + row0, vb, &full[s]);
-      if (SK == SK_COUNT && lane == 0)
-        ptx::bulk_g2s(st + (ncolV + ncolQ) * S, a.code + row0, cb, &full[s]);
     }
   } else {
-    // ---------------------------------------------------------- consumers
     // update coefficients as DMMA B fragments:  B[kk][j] = -C[c0+kk][nj*8+j]
     double cfr[UPD ? MQT * 2 : 1][NT];
     if (UPD) {
@@ -261,192 +340,228 @@ __global__ void __launch_bounds__(kThreads, 1) pass_kernel(const PassArgs a) {
 #pragma unroll
       for (int j = 0; j < NT; ++j) accs[i][j][0] = accs[i][j][1] = 0.0;
 
-    for (int it = 0; it < my_tiles; ++it) {
-      const int s = it % NS;
-      const long long row0 = (long long)(blockIdx.x + (long long)it * gridDim.x) * T;
-      const int valid = (int)(nrows - row0 < T ? nrows - row0 : T);
-      double* st = stages + (size_t)s * stage_dbl;
-      const double* stV = st;
-      const double* stQ = st + ncolV * S;
-      const double* stT = st + (ncolV + ncolQ) * S;
-      const uint32_t* stC = reinterpret_cast<const uint32_t*>(st + (ncolV + ncolQ) * S);
-      double* xt = xtile + (it & 1) * K * S;
+    const bool in_trsm_group = SPLIT && warp < GAW;
+    const int gw = warp - GAW;  // warp index within the U/S/R group
+    const int gtid = gw * 32 + lane;
 
-      if (STORE && tid < K) ptx::bulk_wait_read0();  // previous tile's store drained its X buffer
-      ptx::mbar_wait(&full[s], (it / NS) & 1);
+    if (in_trsm_group) {
+      // ---------------------------------------------- A: row solves (warps 0-3)
+      for (int it = 0; it < my_tiles; ++it) {
+        const int s = it % NS, b = it & 1;
+        const long long row0 = (long long)(blockIdx.x + (long long)it * gridDim.x) * T;
+        const int valid = (int)(nrows - row0 < T ? nrows - row0 : T);
+        const double* stV = stages + (size_t)s * L.stage + L.offV;
+        double* xt = xtile + b * K * S;
+        ptx::mbar_wait(&full[s], (it / NS) & 1);
+        if (it >= 2) ptx::named_bar_sync(4 + b, NW * 32);  // X buffer b drained by the U/S/R group
+        {
+          constexpr int GAWX = GAW ? GAW : 1;
+          constexpr int RPT = (T + GAWX * 32 - 1) / (GAWX * 32);  // rows per thread
+          double x[RPT][kMaxK];
+#pragma unroll
+          for (int q = 0; q < RPT; ++q) {
+            const int r = tid + q * GAWX * 32;
+#pragma unroll
+            for (int c = 0; c < kMaxK; ++c) x[q][c] = (c < K && r < T) ? stV[c * S + r] : 0.0;
+          }
+          row_trsm_n<EXACT, KC, RPT>(x, rfac, rinv, K);
+          if (NPRE > 1) row_trsm_n<EXACT, KC, RPT>(x, rfac + 256, rinv + 16, K);
+#pragma unroll
+          for (int q = 0; q < RPT; ++q) {
+            const int r = tid + q * GAWX * 32;
+            if (r < T) {
+#pragma unroll
+              for (int c = 0; c < kMaxK; ++c)
+                if (c < K) xt[c * S + r] = (r < valid) ? x[q][c] : 0.0;
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&empty[s]);
+        ptx::named_bar_arrive(2 + b, NW * 32);  // X buffer b full
+      }
+      for (int it = (my_tiles >= 2 ? my_tiles - 2 : 0); it < my_tiles; ++it)
+        ptx::named_bar_sync(4 + (it & 1), NW * 32);  // consume the trailing drain signals
+    } else {
+      // ------------------------------------------- U / A' / S / R group
+      for (int it = 0; it < my_tiles; ++it) {
+        const int s = it % NS, b = it & 1;
+        const long long row0 = (long long)(blockIdx.x + (long long)it * gridDim.x) * T;
+        const int valid = (int)(nrows - row0 < T ? nrows - row0 : T);
+        double* st = stages + (size_t)s * L.stage;
+        const double* stV = st + L.offV;
+        const double* stQ = st + L.offQ;
+        const double* stT = st + L.offT;
+        const uint32_t* stC = reinterpret_cast<const uint32_t*>(st + L.offC);
+        double* xt = xtile + b * K * S;
 
-      // ---- A: pre-TRSM, thread per row
-      if (NPRE > 0) {
-        if (tid < T) {
-          const int r = tid;
-          double x[kMaxK];
+        if (!SPLIT && STORE && gtid < K) ptx::bulk_wait_read0();  // previous tile's store drained
+        ptx::mbar_wait(&full[s], (it / NS) & 1);
+        if (SPLIT) ptx::named_bar_sync(2 + b, NW * 32);  // solved rows of this tile are in xt
+
+        // ---- U: X = X0 - Q C on tensor cores
+        if (UPD) {
+          const double* x0 = SPLIT ? xt : stV;
+          for (int rg = gw; rg < T / 8; rg += GW) {
+            const int r = rg * 8 + g;
+            const bool rv = r < valid;
+            double d[NT][2];
 #pragma unroll
-          for (int c = 0; c < kMaxK; ++c) x[c] = (c < K && r < valid) ? stV[c * S + r] : 0.0;
+            for (int nj = 0; nj < NT; ++nj)
 #pragma unroll
-          for (int f = 0; f < NPRE; ++f) {
-            const double* R = rfac + f * 256;
-#pragma unroll
-            for (int j = 0; j < kMaxK; ++j) {
-              if (j < K) {
-#pragma unroll
-                for (int i = 0; i < j; ++i) {
-                  const double rij = R[i + j * kRld];
-                  if (rij != 0.0) x[j] = tiny::sub(x[j], tiny::mul(rij, x[i]));
-                }
-                x[j] = tiny::div(x[j], R[j + j * kRld]);
+              for (int e = 0; e < 2; ++e) {
+                const int c = nj * 8 + 2 * t4 + e;
+                d[nj][e] = (rv && c < K) ? x0[c * S + r] : 0.0;
               }
-            }
-          }
 #pragma unroll
-          for (int c = 0; c < kMaxK; ++c)
-            if (c < K) xt[c * S + r] = (r < valid) ? x[c] : 0.0;
-        }
-        ptx::named_bar_sync(1, NC);
-      }
-
-      // ---- U: X = X0 - Q C on tensor cores, one 8-row group per warp step
-      if (UPD) {
-        const double* x0 = (NPRE > 0) ? xt : stV;
-        for (int rg = warp; rg < T / 8; rg += NW) {
-          const int r = rg * 8 + g;
-          const bool rv = r < valid;
-          double d[NT][2];
-#pragma unroll
-          for (int nj = 0; nj < NT; ++nj)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int c = nj * 8 + 2 * t4 + e;
-              d[nj][e] = (rv && c < K) ? x0[c * S + r] : 0.0;
-            }
-#pragma unroll
-          for (int ks = 0; ks < MQT * 2; ++ks) {
-            if (ks * 4 < p) {
-              const int c = ks * 4 + t4;
-              const double av = (rv && c < p) ? stQ[c * S + r] : 0.0;
-#pragma unroll
-              for (int nj = 0; nj < NT; ++nj) ptx::dmma(d[nj][0], d[nj][1], av, cfr[ks][nj]);
-            }
-          }
-#pragma unroll
-          for (int nj = 0; nj < NT; ++nj)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int c = nj * 8 + 2 * t4 + e;
-              if (c < K) xt[c * S + r] = rv ? d[nj][e] : 0.0;
-            }
-        }
-        ptx::named_bar_sync(1, NC);
-      }
-
-      // ---- A': post-TRSM
-      if (NPOST > 0) {
-        if (tid < T) {
-          const int r = tid;
-          double x[kMaxK];
-#pragma unroll
-          for (int c = 0; c < kMaxK; ++c) x[c] = (c < K) ? xt[c * S + r] : 0.0;
-          const double* R = rfac + 512;
-#pragma unroll
-          for (int j = 0; j < kMaxK; ++j) {
-            if (j < K) {
-#pragma unroll
-              for (int i = 0; i < j; ++i) {
-                const double rij = R[i + j * kRld];
-                if (rij != 0.0) x[j] = tiny::sub(x[j], tiny::mul(rij, x[i]));
-              }
-              x[j] = tiny::div(x[j], R[j + j * kRld]);
-            }
-          }
-#pragma unroll
-          for (int c = 0; c < kMaxK; ++c)
-            if (c < K) xt[c * S + r] = (r < valid) ? x[c] : 0.0;
-        }
-        ptx::named_bar_sync(1, NC);
-      }
-
-      const double* X = XT ? xt : stV;
-
-      // ---- S: bulk store of the X tile
-      if (STORE && tid < K) {
-        ptx::fence_proxy_async_smem();
-        ptx::bulk_s2g(a.out + (long long)tid * a.ldo + row0, xt + tid * S, (uint32_t)(((valid + 1) & ~1) * 8));
-        ptx::bulk_commit();
-      }
-
-      // ---- R: contractions on tensor cores, one 4-row k-step per warp step
-      if (QTX || GRAM || SK == SK_GAUSS) {
-        for (int ks = warp; ks < T / 4; ks += NW) {
-          const int r = ks * 4 + t4;
-          const bool rv = r < valid;
-          double bx[NT];
-#pragma unroll
-          for (int nj = 0; nj < NT; ++nj) {
-            const int c = nj * 8 + g;
-            bx[nj] = (rv && c < K) ? X[c * S + r] : 0.0;
-          }
-          if (QTX) {
-#pragma unroll
-            for (int mi = 0; mi < MQT; ++mi) {
-              if (mi * 8 < p) {
-                const int c = mi * 8 + g;
+            for (int ks = 0; ks < MQT * 2; ++ks) {
+              if (ks * 4 < p) {
+                const int c = ks * 4 + t4;
                 const double av = (rv && c < p) ? stQ[c * S + r] : 0.0;
 #pragma unroll
-                for (int nj = 0; nj < NT; ++nj) ptx::dmma(accq[mi][nj][0], accq[mi][nj][1], av, bx[nj]);
+                for (int nj = 0; nj < NT; ++nj) ptx::dmma(d[nj][0], d[nj][1], av, cfr[ks][nj]);
               }
             }
+#pragma unroll
+            for (int nj = 0; nj < NT; ++nj)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int c = nj * 8 + 2 * t4 + e;
+                if (c < K) xt[c * S + r] = rv ? d[nj][e] : 0.0;
+              }
           }
-          if (GRAM) {
+          ptx::named_bar_sync(GBAR, GT);
+        }
+
+        // ---- A': post-TRSM (thread per row)
+        if (NPOST > 0) {
+          for (int r = gtid; r < T; r += GT) {
+            double x[kMaxK];
 #pragma unroll
-            for (int mi = 0; mi < NT; ++mi)
+            for (int c = 0; c < kMaxK; ++c) x[c] = (c < K) ? xt[c * S + r] : 0.0;
+            row_trsm<EXACT, KC>(x, rfac + 512, rinv + 32, K);
 #pragma unroll
-              for (int nj = 0; nj < NT; ++nj)
-                if (mi <= nj) ptx::dmma(accg[mi][nj][0], accg[mi][nj][1], bx[mi], bx[nj]);
+            for (int c = 0; c < kMaxK; ++c)
+              if (c < K) xt[c * S + r] = (r < valid) ? x[c] : 0.0;
           }
-          if (SK == SK_GAUSS) {
+          ptx::named_bar_sync(GBAR, GT);
+        }
+
+        const double* X = XT ? xt : stV;
+
+        // ---- S: bulk store of the X tile (one request per column)
+        if (STORE && gtid < K) {
+          ptx::fence_proxy_async_smem();
+          ptx::bulk_s2g(a.out + (long long)gtid * a.ldo + row0, xt + gtid * S,
+                        (uint32_t)(((valid + 1) & ~1) * 8));
+          ptx::bulk_commit();
+        }
+
+        // ---- R: contractions on tensor cores, one 4-row k-step per warp step
+        if (QTX || GRAM || SK == SK_GAUSS) {
+          // fragments of k-step ks+GW are loaded while the DMMAs of ks issue
+          constexpr int NQ = QTX ? MQT : 1, NS2 = (SK == SK_GAUSS) ? MST : 1;
+          double bx[2][NT], aq[2][NQ], at[2][NS2];
+          auto load = [&](int ks, int slot) {
+            const int r = ks * 4 + t4;
+            const bool rv = r < valid;
 #pragma unroll
-            for (int mi = 0; mi < MST; ++mi) {
-              if (mi * 8 < mh) {
+            for (int nj = 0; nj < NT; ++nj) {
+              const int c = nj * 8 + g;
+              bx[slot][nj] = (rv && c < K) ? X[c * S + r] : 0.0;
+            }
+            if (QTX) {
+#pragma unroll
+              for (int mi = 0; mi < NQ; ++mi) {
                 const int c = mi * 8 + g;
-                const double av = (rv && c < mh) ? stT[c * S + r] : 0.0;
+                aq[slot][mi] = (mi * 8 < p && rv && c < p) ? stQ[c * S + r] : 0.0;
+              }
+            }
+            if (SK == SK_GAUSS) {
 #pragma unroll
-                for (int nj = 0; nj < NT; ++nj) ptx::dmma(accs[mi][nj][0], accs[mi][nj][1], av, bx[nj]);
+              for (int mi = 0; mi < NS2; ++mi) {
+                const int c = mi * 8 + g;
+                at[slot][mi] = (mi * 8 < mh && rv && c < mh) ? stT[c * S + r] : 0.0;
+              }
+            }
+          };
+          auto mma = [&](int slot) {
+            if (QTX) {
+#pragma unroll
+              for (int mi = 0; mi < NQ; ++mi)
+                if (mi * 8 < p) {
+#pragma unroll
+                  for (int nj = 0; nj < NT; ++nj)
+                    ptx::dmma(accq[mi][nj][0], accq[mi][nj][1], aq[slot][mi], bx[slot][nj]);
+                }
+            }
+            if (GRAM) {
+#pragma unroll
+              for (int mi = 0; mi < NT; ++mi)
+#pragma unroll
+                for (int nj = 0; nj < NT; ++nj)
+                  if (mi <= nj) ptx::dmma(accg[mi][nj][0], accg[mi][nj][1], bx[slot][mi], bx[slot][nj]);
+            }
+            if (SK == SK_GAUSS) {
+#pragma unroll
+              for (int mi = 0; mi < NS2; ++mi)
+                if (mi * 8 < mh) {
+#pragma unroll
+                  for (int nj = 0; nj < NT; ++nj)
+                    ptx::dmma(accs[mi][nj][0], accs[mi][nj][1], at[slot][mi], bx[slot][nj]);
+                }
+            }
+          };
+          // two-slot ring unrolled by hand so that fragment indices stay static
+          int ks = gw;
+          if (ks < T / 4) load(ks, 0);
+          while (ks < T / 4) {
+            if (ks + GW < T / 4) load(ks + GW, 1);
+            mma(0);
+            ks += GW;
+            if (ks >= T / 4) break;
+            if (ks + GW < T / 4) load(ks + GW, 0);
+            mma(1);
+            ks += GW;
+          }
+        }
+        if (SK == SK_COUNT) {
+          // deterministic scatter: warp gw owns buckets b % GW == gw; rows of a
+          // bucket are added in ascending row order (proj/src/sketch.cpp:54-58)
+          for (int g32 = 0; g32 < T / 32; ++g32) {
+            const int r = g32 * 32 + lane;
+            const bool rv = r < valid;
+            const uint32_t code = rv ? stC[r] : 0u;
+            const int bk = (int)(code & 0x7fffffffu);
+            const bool mine = rv && (bk % GW) == gw;
+            const unsigned key = mine ? (unsigned)bk : (0x80000000u | (unsigned)lane);
+            const unsigned grp = __match_any_sync(0xffffffffu, key);
+            if (mine && (__ffs(grp) - 1) == lane) {
+              unsigned m = grp;
+              while (m) {
+                const int q = __ffs(m) - 1;
+                m &= m - 1;
+                const int rq = g32 * 32 + q;
+                const double sg = (stC[rq] & 0x80000000u) ? -1.0 : 1.0;
+                for (int c = 0; c < K; ++c)
+                  cacc[bk + c * mh] = tiny::add(cacc[bk + c * mh], tiny::mul(sg, X[c * S + rq]));
               }
             }
           }
         }
-      }
-      if (SK == SK_COUNT) {
-        // deterministic scatter: warp w owns buckets b % NW == w; rows of a
-        // bucket are added in ascending row order (proj/src/sketch.cpp:54-58)
-        for (int g32 = 0; g32 < T / 32; ++g32) {
-          const int r = g32 * 32 + lane;
-          const bool rv = r < valid;
-          const uint32_t code = rv ? stC[r] : 0u;
-          const int b = (int)(code & 0x7fffffffu);
-          const bool mine = rv && (b % NW) == warp;
-          const unsigned key = mine ? (unsigned)b : (0x80000000u | (unsigned)lane);
-          const unsigned grp = __match_any_sync(0xffffffffu, key);
-          if (mine && (__ffs(grp) - 1) == lane) {
-            unsigned m = grp;
-            while (m) {
-              const int q = __ffs(m) - 1;
-              m &= m - 1;
-              const int rq = g32 * 32 + q;
-              const double sg = (stC[rq] & 0x80000000u) ? -1.0 : 1.0;
-              for (int c = 0; c < K; ++c)
-                cacc[b + c * mh] = tiny::add(cacc[b + c * mh], tiny::mul(sg, X[c * S + rq]));
-            }
-          }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&empty[s]);
+        if (SPLIT) {
+          if (STORE && gtid < K) ptx::bulk_wait_read0();
+          ptx::named_bar_arrive(4 + b, NW * 32);  // X buffer b may be refilled
         }
       }
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&empty[s]);
+      if (STORE && gtid < K) ptx::bulk_wait0();
     }
-    if (STORE && tid < K) ptx::bulk_wait0();
 
     // ---- per-warp fragments -> shared, then fixed-order sum over warps
-    ptx::named_bar_sync(1, NC);  // all stages consumed: reuse stage memory
-    double* red = stages;        // [NW][dm_len]
+    ptx::named_bar_sync(1, NW * 32);  // all stages consumed: reuse stage memory
+    double* red = stages;             // [NW][dm_len]
     const int dm_len = a.dm_len;
     for (int e = lane; e < dm_len; e += 32) red[warp * dm_len + e] = 0.0;
     __syncwarp();
@@ -486,15 +601,15 @@ __global__ void __launch_bounds__(kThreads, 1) pass_kernel(const PassArgs a) {
             if (i < a.ld_s && j < 16) red[warp * dm_len + a.off_s + i + j * a.ld_s] = accs[mi][nj][e];
           }
     }
-    ptx::named_bar_sync(1, NC);
+    ptx::named_bar_sync(1, NW * 32);
     double* part = a.partials + (size_t)blockIdx.x * a.part_len;
-    for (int e = tid; e < dm_len; e += NC) {
+    for (int e = tid; e < dm_len; e += NW * 32) {
       double sum = 0.0;
       for (int w = 0; w < NW; ++w) sum += red[w * dm_len + e];
       part[e] = sum;
     }
     if (SK == SK_COUNT) {
-      for (int e = tid; e < mh * K; e += NC) {
+      for (int e = tid; e < mh * K; e += NW * 32) {
         const int i = e % mh, j = e / mh;
         part[a.off_s + i + j * a.ld_s] = cacc[e];
       }
