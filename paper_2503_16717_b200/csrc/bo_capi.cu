@@ -71,17 +71,6 @@ void ok_st(bo_status* st) {
 // ---------------------------------------------------------------------------
 // NCCL, loaded lazily (prefer the copy torch already mapped)
 // ---------------------------------------------------------------------------
-typedef int (*nccl_get_id_t)(void*);
-typedef int (*nccl_init_rank_t)(void**, int, const void* /*by value struct*/, int);
-struct NcclApi {
-  void* h = nullptr;
-  int (*GetUniqueId)(void* id) = nullptr;
-  int (*CommInitRank)(void** comm, int nranks, char id[128], int rank) = nullptr;
-  int (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
-  int (*CommDestroy)(void*) = nullptr;
-  const char* (*GetErrorString)(int) = nullptr;
-  bool ok = false;
-};
 NcclApi& nccl() {
   static NcclApi api;
   static std::once_flag once;
@@ -103,12 +92,15 @@ NcclApi& nccl() {
         api.h, "ncclAllReduce");
     api.CommDestroy = (int (*)(void*))dlsym(api.h, "ncclCommDestroy");
     api.GetErrorString = (const char* (*)(int))dlsym(api.h, "ncclGetErrorString");
+    api.Send = (int (*)(const void*, size_t, int, int, void*, cudaStream_t))dlsym(api.h, "ncclSend");
+    api.Recv = (int (*)(void*, size_t, int, int, void*, cudaStream_t))dlsym(api.h, "ncclRecv");
+    api.GroupStart = (int (*)())dlsym(api.h, "ncclGroupStart");
+    api.GroupEnd = (int (*)())dlsym(api.h, "ncclGroupEnd");
+    api.AllGather = (int (*)(const void*, void*, size_t, int, void*, cudaStream_t))dlsym(api.h, "ncclAllGather");
     api.ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.CommDestroy;
   });
   return api;
 }
-constexpr int kNcclFloat64 = 8;  // ncclDouble
-constexpr int kNcclSum = 0;
 
 }  // namespace host
 }  // namespace bo
@@ -196,7 +188,7 @@ PassFn get_pass_fn(int nt, int T, int kind, bool exact, int K) {
 }
 
 // launch one streaming pass (+ its reduction / finalize) on the ctx stream
-int run_pass(bo_ctx ctx, PassReq& r, bo_status* st) {
+int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st) {
   const KindInfo& ki = kKindInfo[r.kind];
   PassArgs a{};
   a.nrows = (long long)ctx->n_local;
@@ -221,9 +213,10 @@ int run_pass(bo_ctx ctx, PassReq& r, bo_status* st) {
     mh = (int)r.sk->mhat;
   } else if (ki.sk == SK_COUNT) {
     a.code = r.sk->code;
-    mh = (int)r.sk->mc;
+    mh = r.bucket_n ? r.bucket_n : (int)r.sk->mc;
   }
   a.mh = mh;
+  a.bucket_lo = r.bucket_lo;
   if (r.p > kMaxPTile) return set_st(st, BO_INVALID, 0, 0.0, "projection range of %d columns exceeds %d", r.p, kMaxPTile);
   if (r.K < 1 || r.K > kMaxK) return set_st(st, BO_INVALID, 0, 0.0, "panel width %d outside [1, %d]", r.K, kMaxK);
   if (ki.sk == SK_GAUSS && mh > 32) return set_st(st, BO_INVALID, 0, 0.0, "gaussian sketch of %d rows exceeds 32", mh);
@@ -300,6 +293,7 @@ int run_pass(bo_ctx ctx, PassReq& r, bo_status* st) {
   FinArgs& f = r.fin;
   f.K = r.K;
   f.p = r.p;
+  if (f.p_total == 0) f.p_total = r.p;
   f.mh = (ki.sk == SK_COUNT && r.sk && r.sk->theta_g) ? (int)r.sk->mhat : mh;
   f.mc = (ki.sk == SK_COUNT && r.sk) ? (int)r.sk->mc : 0;
   f.theta_g = (ki.sk == SK_COUNT && r.sk) ? r.sk->theta_g : nullptr;
@@ -374,6 +368,48 @@ int run_pass(bo_ctx ctx, PassReq& r, bo_status* st) {
   return BO_OK;
 }
 
+
+
+// Projection ranges wider than one pass (64 columns) are split into column
+// chunks: Q^T X chunk by chunk into the rows of Cq; X = V - Q C as a chain of
+// partial updates through the output buffer, the last chunk carrying the
+// pass's own reductions and finalize.
+int run_pass(bo_ctx ctx, PassReq& r, bo_status* st) {
+  const KindInfo& ki = kKindInfo[r.kind];
+  if (!(ki.qtx || ki.upd) || r.p <= kMaxPTile) return run_pass_single(ctx, r, st);
+  const int P = r.p;
+  for (int c0 = 0; c0 < P; c0 += kMaxPTile) {
+    const bool last = c0 + kMaxPTile >= P;
+    PassReq q = r;
+    q.Q = r.Q + (size_t)c0 * r.ldq;
+    q.p = std::min(kMaxPTile, P - c0);
+    q.fin.p_total = P;
+    if (ki.qtx) {
+      q.fin.q_row_off = c0;
+      if (!last) {
+        q.kind = ki.npre == 2 ? PK_P2_QTX : PK_QTX;
+        q.fin.ops = FIN_COPY_Q;
+      }
+    } else {
+      q.Cm = r.Cm + c0;
+      if (c0 > 0) {  // continue from the partial update stored by the previous chunk
+        q.V = r.out;
+        q.ldv = r.ldo;
+        q.Rpre0 = q.Rpre1 = nullptr;
+      }
+      if (!last) {
+        q.kind = (c0 == 0 && ki.npre == 2) ? PK_P2_UPD_ST : PK_UPD_ST;
+        q.fin.ops = 0;
+        q.sk = nullptr;
+      } else if (c0 > 0 && ki.npre == 2) {
+        q.kind = PK_UPD_GRAM_ST;  // the only pre-solve update kind (P2_UPD_GRAM_ST) minus its solve
+      }
+      if (!r.out) return set_st(st, BO_INVALID, 0, 0.0, "chunked update needs an output buffer");
+    }
+    TRY(run_pass_single(ctx, q, st));
+  }
+  return BO_OK;
+}
 
 // zero the device status word
 int reset_status(bo_ctx ctx, bo_status* st) {
@@ -841,11 +877,9 @@ extern "C" int bo_sketch_apply(bo_sketch sk, const double* v, uint64_t ldv, uint
   const double* vv;
   uint64_t lv;
   TRY(stage_input(ctx, v, ldv, k, 0, &vv, &lv, st));
-  TRY(reset_status(ctx, st));
-  TRY(sketch_pass(sk, vv, lv, (int)k, 1, 0, st));
-  TRY(fetch(ctx, true, st));
-  const double* S = ctx->tiny_host + OFF_S;
-  std::memcpy(out, S, sk->mhat * k * 8);
+  std::vector<double> S;
+  TRY(sketch_to_host(sk, vv, lv, (int)k, S, st));
+  std::memcpy(out, S.data(), sk->mhat * k * 8);
   if (ledger) ledger[BO_LEDGER_SKETCH]++;
   return BO_OK;
 }

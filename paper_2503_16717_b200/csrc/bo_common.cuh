@@ -62,7 +62,9 @@ enum FinOp : int {
 
 struct FinArgs {
   int ops;
-  int K, p, mh, mc;        // panel width, QTX rows, sketch rows, count width (count-gauss)
+  int K, p, mh, mc;        // panel width, QTX rows of this pass, sketch rows, count width (count-gauss)
+  int p_total;             // rows of the full projection block (chunked passes), >= q_row_off + p
+  int q_row_off;           // row offset of this pass's QTX block inside Cq
   int pass_id;
   double pivot_tol;
   const double* sums;      // reduced partials
@@ -99,7 +101,8 @@ struct PassArgs {
   const double* Th;        // gaussian sketch rows (local rows x mh)
   long long ldth;
   const uint32_t* code;    // count sketch: bucket | sign bit (local rows)
-  int mh;                  // sketch rows (gauss) / buckets (count)
+  int mh;                  // sketch rows (gauss) / buckets of this pass (count)
+  int bucket_lo;           // count: first bucket handled by this pass
   double* out;
   long long ldo;
   const double* Rpre0;     // first pre-TRSM factor (16 x 16)

@@ -82,7 +82,9 @@ struct bo_op_s {
   double a_fro = 0.0;      // ||A||_F (global)
   // halo (world > 1): rows needed below/above the shard
   uint64_t halo_lo = 0, halo_hi = 0;
+  uint64_t peer_need_lo = 0, peer_need_hi = 0;  // rows the neighbours need from us
   double* xext = nullptr;  // extended x: [halo_lo | local | halo_hi]
+  double a_fro_local2 = 0.0;  // sum of squared values of this shard's rows
 };
 
 namespace bo {
@@ -104,7 +106,8 @@ namespace host {
   X(P2_UPD_GRAM_ST, 2, true, 0, false, true, SK_NONE, true)            \
   X(P1_ST, 1, false, 0, false, false, SK_NONE, true)                   \
   X(P2_ST, 2, false, 0, false, false, SK_NONE, true)                    \
-  X(UPD_POST_ST, 0, true, 1, false, false, SK_NONE, true)
+  X(UPD_POST_ST, 0, true, 1, false, false, SK_NONE, true)              \
+  X(P2_UPD_ST, 2, true, 0, false, false, SK_NONE, true)
 
 enum PassKind {
 #define X(nm, a, b, c, d, e, f, g) PK_##nm,
@@ -144,18 +147,42 @@ struct PassReq {
   FinArgs fin{};
   int pass_id = 0;
   bool exact = false;  // bit-exact substitution (standalone apply_inv_upper only)
+  int bucket_lo = 0;   // count sketch: first bucket of this pass (chunked bucket ranges)
+  int bucket_n = 0;    // buckets in this pass (0 = all)
 };
 
 
 // tiny workspace layout (doubles) — all K x K factors have ld 16
+// projection coefficient blocks (p x K) have ld LDC = 256 (p <= 255 basis columns)
+constexpr int LDC = 256;
 constexpr int OFF_R1 = 0, OFF_R2 = 256, OFF_R3 = 512, OFF_RIN = 768, OFF_RJJ = 1024,
-              OFF_G = 1280, OFF_R4 = 1536, OFF_C1 = 2048, OFF_C2 = 3072, OFF_COEF = 4096,
-              OFF_S = 5120, TINY_LEN = 5120 + 8192;
-constexpr int LDC = 64;
+              OFF_G = 1280, OFF_R4 = 1536, OFF_C1 = 2048, OFF_C2 = OFF_C1 + LDC * 16,
+              OFF_COEF = OFF_C2 + LDC * 16, OFF_S = OFF_COEF + LDC * 16, TINY_LEN = OFF_S + 8192;
+
+// NCCL, loaded lazily with dlopen (prefers the copy torch already mapped)
+struct NcclApi {
+  void* h = nullptr;
+  int (*GetUniqueId)(void* id) = nullptr;
+  int (*CommInitRank)(void** comm, int nranks, char id[128], int rank) = nullptr;
+  int (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*CommDestroy)(void*) = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+  int (*Send)(const void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*Recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*GroupStart)() = nullptr;
+  int (*GroupEnd)() = nullptr;
+  int (*AllGather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
+  bool ok = false;
+};
+NcclApi& nccl();
+constexpr int kNcclFloat64 = 8;  // ncclDouble
+constexpr int kNcclUint64 = 5;   // ncclUint64
+constexpr int kNcclSum = 0;
 
 int set_st(bo_status* st, int code, long long index, double pivot, const char* fmt, ...);
 void ok_st(bo_status* st);
-int run_pass(bo_ctx ctx, PassReq& r, bo_status* st);
+int run_pass(bo_ctx ctx, PassReq& r, bo_status* st);        // splits p > 64 into chunks
+int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st);
 inline double* T_(bo_ctx ctx, int off) { return ctx->tiny + off; }
 int reset_status(bo_ctx ctx, bo_status* st);
 int fetch(bo_ctx ctx, bool tiny, bo_status* st);
@@ -173,6 +200,8 @@ int sketch_pass(bo_sketch sk, const double* v, uint64_t ldv, int K, int pass_id,
 void push_panel_host(bo_basis b, uint64_t k, const double* proj, uint64_t ldp, const double* diag, uint64_t ldd,
                      bool overlap);
 uint64_t derive_seed(uint64_t base, uint64_t stream);
+int op_apply(bo_op op, const double* x, double* y, bo_status* st);
+int sketch_to_host(bo_sketch th, const double* v, uint64_t ldv, int K, std::vector<double>& S, bo_status* st);
 inline uint64_t round_up(uint64_t x, uint64_t m) { return (x + m - 1) / m * m; }
 
 }  // namespace host

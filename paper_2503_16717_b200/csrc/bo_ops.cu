@@ -1,1 +1,1103 @@
+// bo_ops.cu — the rest of the hot-path surface over the streaming-pass engine:
+//   * matrix-powers kernel: CSR (int32) and matrix-free Laplacian SpMV,
+//     bit-exact with proj/src/sparse.cpp:51-63, with NCCL halo exchange
+//   * recursive CholQR breakdown recovery (proj/src/intra_orth.cpp:43-139)
+//   * BCGS-PIP and RandBCGS preprocessing (proj/src/block_orth.cpp:230-336)
+//   * two-stage panel / finish (proj/src/block_orth.cpp:338-389), whose big
+//     panel (up to 64 columns) uses the wide contraction / solve kernels here.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "bo_hostdense.h"
 #include "bo_internal.h"
+#include "bo_ptx.cuh"
+
+
+using namespace bo;
+using namespace bo::host;
+
+#define CU(call)                                                                            \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return set_st(st, BO_CUDA, 0, 0.0, "CUDA error %s at %s:%d", cudaGetErrorString(e_), \
+                    __FILE__, __LINE__);                                                    \
+  } while (0)
+#define TRY(expr)                 \
+  do {                            \
+    int rc_ = (expr);             \
+    if (rc_ != BO_OK) return rc_; \
+  } while (0)
+
+namespace bo {
+
+// ===========================================================================
+// SpMV kernels
+// ===========================================================================
+// y_r = sum_k val[k] * x[col[k]], sequential ascending-column sum from +0.0 with
+// unfused mul/add: bit-identical to proj/src/sparse.cpp:57-61.
+__global__ void __launch_bounds__(256) spmv_csr_kernel(long long nrows, const int* __restrict__ rp,
+                                                       const int* __restrict__ col,
+                                                       const double* __restrict__ val,
+                                                       const double* __restrict__ x, double* __restrict__ y) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < nrows; r += (long long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    const int e = rp[r + 1];
+    for (int k = rp[r]; k < e; ++k) s = __dadd_rn(s, __dmul_rn(__ldg(val + k), __ldg(x + col[k])));
+    y[r] = s;
+  }
+}
+
+// Matrix-free 2D 5-point / 3D 7-point Laplacian (problems.cpp:65-113): same
+// entries, same ascending-column order, so bit-identical to the CSR SpMV.
+// xext holds [halo_lo rows | local rows | halo_hi rows].
+__global__ void __launch_bounds__(256) spmv_laplace_kernel(int dims, long long k, long long row_begin,
+                                                           long long nrows, long long halo_lo,
+                                                           const double* __restrict__ xext,
+                                                           double* __restrict__ y) {
+  const double diag = dims == 2 ? 4.0 : 6.0;
+  const long long off = row_begin - halo_lo;  // xext index = global - off
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < nrows; r += (long long)gridDim.x * blockDim.x) {
+    const long long me = row_begin + r;
+    double s = 0.0;
+    if (dims == 3) {
+      const long long kk = k * k;
+      const long long i = me / kk, j = (me / k) % k, l = me % k;
+      if (i > 0) s = __dadd_rn(s, __dmul_rn(-1.0, xext[me - kk - off]));
+      if (j > 0) s = __dadd_rn(s, __dmul_rn(-1.0, xext[me - k - off]));
+      if (l > 0) s = __dadd_rn(s, __dmul_rn(-1.0, xext[me - 1 - off]));
+      s = __dadd_rn(s, __dmul_rn(diag, xext[me - off]));
+      if (l + 1 < k) s = __dadd_rn(s, __dmul_rn(-1.0, xext[me + 1 - off]));
+      if (j + 1 < k) s = __dadd_rn(s, __dmul_rn(-1.0, xext[me + k - off]));
+      if (i + 1 < k) s = __dadd_rn(s, __dmul_rn(-1.0, xext[me + kk - off]));
+    } else {
+      const long long i = me / k, j = me % k;
+      if (i > 0) s = __dadd_rn(s, __dmul_rn(-1.0, xext[me - k - off]));
+      if (j > 0) s = __dadd_rn(s, __dmul_rn(-1.0, xext[me - 1 - off]));
+      s = __dadd_rn(s, __dmul_rn(diag, xext[me - off]));
+      if (j + 1 < k) s = __dadd_rn(s, __dmul_rn(-1.0, xext[me + 1 - off]));
+      if (i + 1 < k) s = __dadd_rn(s, __dmul_rn(-1.0, xext[me + k - off]));
+    }
+    y[r] = s;
+  }
+}
+
+// ===========================================================================
+// wide (<= 64 column) contraction and solve kernels for the two-stage big panel
+// ===========================================================================
+struct WideArgs {
+  long long nrows;
+  const double* L;
+  long long ldl;
+  int ml;
+  const double* X;
+  long long ldx;
+  int kx;
+  int sym;  // L == X: only upper tiles
+  double* partials;  // [grid][64*64]
+  double* sums;      // [64*64]
+  unsigned* counter;
+  DevStatus* status;
+};
+
+// out(ml x kx) = L^T X ; CTA walks 64-row tiles, each warp owns fixed 8x8
+// output tiles (DMMA), last CTA sums the CTA partials in fixed order.
+__global__ void __launch_bounds__(256) wide_contract_kernel(const WideArgs a) {
+  constexpr int TR = 64, S = TR + 4;
+  extern __shared__ __align__(16) double wsm[];
+  double* Ls = wsm;                // [ml][S]
+  double* Xs = wsm + 64 * S;       // [kx][S]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
+  if (a.status->code != ST_OK) return;
+  const int mt = (a.ml + 7) / 8, nt = (a.kx + 7) / 8;
+  int tiles[8][2];
+  int ntile = 0;
+  // valid 8x8 output tiles in row-major order; warp w owns every 8th one
+  for (int idx = 0, cnt = 0; idx < 64; ++idx) {
+    const int mi = idx / 8, nj = idx % 8;
+    if (mi >= mt || nj >= nt || (a.sym && mi > nj)) continue;
+    if (cnt % 8 == warp && ntile < 8) {
+      tiles[ntile][0] = mi;
+      tiles[ntile][1] = nj;
+      ++ntile;
+    }
+    ++cnt;
+  }
+  double acc[8][2];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) acc[q][0] = acc[q][1] = 0.0;
+  const long long ntiles_rows = (a.nrows + TR - 1) / TR;
+  for (long long tr = blockIdx.x; tr < ntiles_rows; tr += gridDim.x) {
+    const long long row0 = tr * TR;
+    __syncthreads();
+    for (int e = tid; e < a.ml * TR; e += blockDim.x) {
+      const int c = e / TR, r = e % TR;
+      Ls[c * S + r] = (row0 + r < a.nrows) ? a.L[c * a.ldl + row0 + r] : 0.0;
+    }
+    if (!a.sym)
+      for (int e = tid; e < a.kx * TR; e += blockDim.x) {
+        const int c = e / TR, r = e % TR;
+        Xs[c * S + r] = (row0 + r < a.nrows) ? a.X[c * a.ldx + row0 + r] : 0.0;
+      }
+    __syncthreads();
+    const double* Xp = a.sym ? Ls : Xs;
+    for (int ks = 0; ks < TR / 4; ++ks) {
+      const int r = ks * 4 + t4;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (q < ntile) {
+          const int ca = tiles[q][0] * 8 + g, cb = tiles[q][1] * 8 + g;
+          const double av = ca < a.ml ? Ls[ca * S + r] : 0.0;
+          const double bv = cb < a.kx ? Xp[cb * S + r] : 0.0;
+          ptx::dmma(acc[q][0], acc[q][1], av, bv);
+        }
+      }
+    }
+  }
+  // CTA partial: every output entry is owned by exactly one warp
+  double* part = a.partials + (size_t)blockIdx.x * 4096;
+  __syncthreads();
+  for (int e = tid; e < 4096; e += blockDim.x) part[e] = 0.0;
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+    if (q < ntile) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = tiles[q][0] * 8 + g, j = tiles[q][1] * 8 + 2 * t4 + e;
+        part[i + j * 64] = acc[q][e];
+        if (a.sym && tiles[q][0] < tiles[q][1]) part[j + i * 64] = acc[q][e];
+      }
+    }
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = (atomicAdd(a.counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int e = tid; e < 4096; e += blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) s += __ldcg(a.partials + (size_t)b * 4096 + e);
+    a.sums[e] = s;
+  }
+  if (tid == 0) *a.counter = 0u;
+}
+
+struct WideUpd {
+  long long nrows;
+  const double* V;
+  long long ldv;
+  int kx;
+  const double* Q;  // optional update  X = V - Q C
+  long long ldq;
+  int p;
+  const double* C;  // p x kx, ld 64
+  const double* R;  // optional solve X R^{-1}, kx x kx, ld 64
+  double* out;
+  long long ldo;
+  DevStatus* status;
+};
+
+// thread per row: X = (V - Q C) R^{-1}, right-looking substitution
+__global__ void __launch_bounds__(128) wide_update_trsm_kernel(const WideUpd a) {
+  extern __shared__ __align__(16) double wus[];
+  double* Cs = wus;              // [64 * 64]
+  double* Rs = wus + 64 * 64;    // [64 * 64]
+  double* rinv = wus + 2 * 64 * 64;
+  if (a.status->code != ST_OK) return;
+  for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) {
+    Cs[e] = a.Q ? a.C[e] : 0.0;
+    Rs[e] = a.R ? a.R[e] : 0.0;
+  }
+  __syncthreads();
+  if (threadIdx.x < 64) rinv[threadIdx.x] = a.R ? 1.0 / Rs[threadIdx.x * 65] : 1.0;
+  __syncthreads();
+  const int kx = a.kx;
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < a.nrows; r += (long long)gridDim.x * blockDim.x) {
+    double x[64];
+#pragma unroll
+    for (int j = 0; j < 64; ++j) x[j] = j < kx ? a.V[j * a.ldv + r] : 0.0;
+    if (a.Q) {
+      for (int i = 0; i < a.p; ++i) {
+        const double q = a.Q[i * a.ldq + r];
+#pragma unroll
+        for (int j = 0; j < 64; ++j)
+          if (j < kx) x[j] = fma(-q, Cs[i + j * 64], x[j]);
+      }
+    }
+    if (a.R) {
+#pragma unroll
+      for (int j = 0; j < 64; ++j) {
+        if (j < kx) {
+          x[j] *= rinv[j];
+#pragma unroll
+          for (int l = j + 1; l < 64; ++l)
+            if (l < kx) x[l] = fma(-Rs[j + l * 64], x[j], x[l]);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 64; ++j)
+      if (j < kx) a.out[j * a.ldo + r] = x[j];
+  }
+}
+
+}  // namespace bo
+
+// ===========================================================================
+// host wrappers
+// ===========================================================================
+namespace {
+
+// L^T X (ml x kx) -> host (column-major ml x kx); allreduced across ranks
+int wide_contract(bo_ctx ctx, const double* L, uint64_t ldl, int ml, const double* X, uint64_t ldx, int kx,
+                  hd::Mat& out, bo_status* st) {
+  if (ml > 64 || kx > 64) return set_st(st, BO_INVALID, 0, 0.0, "wide block of more than 64 columns");
+  const bool sym = (L == X && ml == kx && ldl == ldx);
+  const long long ntr = ((long long)ctx->n_local + 63) / 64;
+  const int grid = (int)std::max<long long>(1, std::min<long long>(ctx->num_sms, ntr));
+  const size_t need = (size_t)grid * 4096;
+  if (need > ctx->partials_cap) {
+    if (ctx->partials) cudaFree(ctx->partials);
+    ctx->partials_cap = need * 2;
+    CU(cudaMalloc(&ctx->partials, ctx->partials_cap * 8));
+  }
+  if (4096 > ctx->sums_cap) {
+    if (ctx->sums) cudaFree(ctx->sums);
+    ctx->sums_cap = 8192;
+    CU(cudaMalloc(&ctx->sums, ctx->sums_cap * 8));
+  }
+  WideArgs a{(long long)ctx->n_local, L, (long long)ldl, ml, X, (long long)ldx, kx, sym ? 1 : 0,
+             ctx->partials, ctx->sums, ctx->counter, ctx->status};
+  const size_t smem = (size_t)2 * 64 * 68 * 8;
+  static bool attr = false;
+  if (!attr) {
+    CU(cudaFuncSetAttribute((const void*)wide_contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  wide_contract_kernel<<<grid, 256, smem, ctx->stream>>>(a);
+  CU(cudaGetLastError());
+  ctx->launches++;
+  if (ctx->world > 1) {
+    NcclApi& nc = nccl();
+    int rc = nc.AllReduce(ctx->sums, ctx->sums, 4096, kNcclFloat64, kNcclSum, ctx->nccl, ctx->stream);
+    if (rc) return set_st(st, BO_NCCL, 0, 0.0, "ncclAllReduce failed (%d)", rc);
+    ctx->allreduces++;
+  }
+  std::vector<double> h(4096);
+  CU(cudaMemcpyAsync(h.data(), ctx->sums, 4096 * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaMemcpyAsync(ctx->status_host, ctx->status, sizeof(DevStatus), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  out = hd::Mat(ml, kx);
+  for (int j = 0; j < kx; ++j)
+    for (int i = 0; i < ml; ++i) out(i, j) = h[i + j * 64];
+  return BO_OK;
+}
+
+// out = (V - Q C) R^{-1} (either part optional), kx <= 64 columns
+int wide_update_trsm(bo_ctx ctx, const double* V, uint64_t ldv, int kx, const double* Q, uint64_t ldq, int p,
+                     const hd::Mat* C, const hd::Mat* R, double* out, uint64_t ldo, bo_status* st) {
+  std::vector<double> hc(4096, 0.0), hr(4096, 0.0);
+  if (C)
+    for (size_t j = 0; j < C->c; ++j)
+      for (size_t i = 0; i < C->r; ++i) hc[i + j * 64] = (*C)(i, j);
+  if (R)
+    for (size_t j = 0; j < R->c; ++j)
+      for (size_t i = 0; i <= j && i < R->r; ++i) hr[i + j * 64] = (*R)(i, j);
+  double* dbuf = nullptr;
+  CU(cudaMallocAsync((void**)&dbuf, 8192 * 8, ctx->stream));
+  CU(cudaMemcpyAsync(dbuf, hc.data(), 4096 * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaMemcpyAsync(dbuf + 4096, hr.data(), 4096 * 8, cudaMemcpyHostToDevice, ctx->stream));
+  WideUpd a{(long long)ctx->n_local, V, (long long)ldv, kx, (Q && p > 0) ? Q : nullptr, (long long)ldq, p,
+            dbuf, R ? dbuf + 4096 : nullptr, out, (long long)ldo, ctx->status};
+  const int grid = (int)std::max<long long>(1, std::min<long long>(ctx->num_sms * 4, ((long long)ctx->n_local + 127) / 128));
+  const size_t smem = (2 * 64 * 64 + 64) * 8;
+  static bool attr = false;
+  if (!attr) {
+    CU(cudaFuncSetAttribute((const void*)wide_update_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem));
+    attr = true;
+  }
+  wide_update_trsm_kernel<<<grid, 128, smem, ctx->stream>>>(a);
+  CU(cudaGetLastError());
+  ctx->launches++;
+  CU(cudaFreeAsync(dbuf, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));  // host vectors must outlive the copies
+  return BO_OK;
+}
+
+// refactor_block / reorthogonalize_block bookkeeping (block_orth.cpp:111-153)
+void refactor_rows(bo_basis b, uint64_t lo, const hd::Mat& t) {
+  const uint64_t w = b->cols - lo, cap = b->cap;
+  std::vector<double> seg(w);
+  auto update = [&](std::vector<double>& m, uint64_t col) {
+    for (uint64_t i = 0; i < w; ++i) seg[i] = m[lo + i + col * cap];
+    for (uint64_t i = 0; i < w; ++i) {
+      double s = 0.0;
+      for (uint64_t l = i; l < w; ++l) s += t(i, l) * seg[l];
+      m[lo + i + col * cap] = s;
+    }
+  };
+  for (uint64_t col = lo; col < b->cols; ++col) {
+    update(b->r, col);
+    if (b->seeded[col]) update(b->c, col);
+  }
+}
+void reorth_rows(bo_basis b, uint64_t lo, const hd::Mat& tproj, const hd::Mat& t) {
+  const uint64_t w = b->cols - lo, cap = b->cap;
+  auto spray = [&](std::vector<double>& m, uint64_t col) {
+    for (uint64_t i = 0; i < lo; ++i) {
+      double s = 0.0;
+      for (uint64_t l = 0; l < w; ++l) s += tproj(i, l) * m[lo + l + col * cap];
+      m[i + col * cap] += s;
+    }
+  };
+  for (uint64_t col = lo; col < b->cols; ++col) {
+    spray(b->r, col);
+    if (b->seeded[col]) spray(b->c, col);
+  }
+  refactor_rows(b, lo, t);
+}
+
+// device cholqr of a wide block in place: Q = V R^{-1} (host Cholesky of the
+// reduced Gram, identical to dense.cpp:75-102); one gram ledger event
+int wide_cholqr(bo_ctx ctx, double* v, uint64_t ldv, int w, const char* chol_ctx, hd::Mat& R, uint64_t* ledger,
+                bo_status* st) {
+  hd::Mat G;
+  TRY(wide_contract(ctx, v, ldv, w, v, ldv, w, G, st));
+  if (ledger) ledger[BO_LEDGER_GRAM]++;
+  double piv = 0.0;
+  const size_t f = hd::cholesky(G, R, 2.220446049250313e-16, &piv);
+  if (f)
+    return set_st(st, BO_CHOLESKY_BREAKDOWN, (long long)f, piv, "%s: nonpositive Cholesky pivot at step %zu",
+                  chol_ctx, f);
+  return wide_update_trsm(ctx, v, ldv, w, nullptr, 0, 0, nullptr, &R, v, ldv, st);
+}
+
+}  // namespace
+
+
+namespace bo {
+namespace host {
+// S = Theta^T V (mhat x K) to host, one sketch ledger event.  Small sketches
+// run fused in one streaming pass; a Gaussian sketch wider than 32 rows (the
+// two-stage shat = 60 case, mhat = 122) goes through the wide contraction in
+// 64-row chunks; a Count stage with thousands of buckets is swept in bucket
+// ranges and the count_gauss dense stage is applied on the host
+// (proj/src/sketch.cpp:110-126; Theta_g is replicated).
+int sketch_to_host(bo_sketch th, const double* v, uint64_t ldv, int K, std::vector<double>& S, bo_status* st) {
+  bo_ctx ctx = th->ctx;
+  const uint64_t mh = th->mhat;
+  S.assign(mh * K, 0.0);
+  const bool small = th->kind == BO_SKETCH_GAUSSIAN ? mh <= 32 : th->mc * (uint64_t)K <= 4096;
+  if (small) {
+    TRY(reset_status(ctx, st));
+    TRY(sketch_pass(th, v, ldv, K, 1, 0, st));
+    TRY(fetch(ctx, true, st));
+    std::memcpy(S.data(), ctx->tiny_host + OFF_S, mh * K * 8);
+    return BO_OK;
+  }
+  if (th->kind == BO_SKETCH_GAUSSIAN) {
+    for (uint64_t c0 = 0; c0 < mh; c0 += 64) {
+      const int rows = (int)std::min<uint64_t>(64, mh - c0);
+      hd::Mat M;
+      TRY(wide_contract(ctx, th->theta + c0 * th->ldth, th->ldth, rows, v, ldv, K, M, st));
+      for (int j = 0; j < K; ++j)
+        for (int i = 0; i < rows; ++i) S[(c0 + i) + j * mh] = M(i, j);
+    }
+    return BO_OK;
+  }
+  const uint64_t mc = th->mc;
+  const int chunk = std::max(64, 4096 / K);
+  std::vector<double> cnt(mc * K, 0.0), hs;
+  for (uint64_t b0 = 0; b0 < mc; b0 += chunk) {
+    const int nb = (int)std::min<uint64_t>(chunk, mc - b0);
+    TRY(reset_status(ctx, st));
+    PassReq r{};
+    r.kind = PK_SKC;
+    r.K = K;
+    r.V = v;
+    r.ldv = ldv;
+    r.sk = th;
+    r.bucket_lo = (int)b0;
+    r.bucket_n = nb;
+    r.fin.ops = 0;
+    TRY(run_pass(ctx, r, st));
+    hs.resize((size_t)nb * 16);
+    CU(cudaMemcpyAsync(hs.data(), ctx->sums, (size_t)nb * 16 * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    for (int j = 0; j < K; ++j)
+      for (int i = 0; i < nb; ++i) cnt[(b0 + i) + j * mc] = hs[i + (size_t)j * nb];
+  }
+  if (th->kind == BO_SKETCH_COUNT) {
+    S = cnt;
+    return BO_OK;
+  }
+  for (int j = 0; j < K; ++j)  // transpose_times(dense, count) order (dense.cpp:28-42)
+    for (uint64_t i = 0; i < mh; ++i) {
+      double s = 0.0;
+      for (uint64_t r = 0; r < mc; ++r) s += th->theta_g_host[r + i * mc] * cnt[r + j * mc];
+      S[i + j * mh] = s;
+    }
+  return BO_OK;
+}
+}  // namespace host
+}  // namespace bo
+
+// ===========================================================================
+// operator / SpMV / MPK
+// ===========================================================================
+namespace {
+int op_setup_halo(bo_op op, long long need_lo, long long need_hi, bo_status* st) {
+  bo_ctx ctx = op->ctx;
+  op->halo_lo = (uint64_t)std::max<long long>(0, (long long)ctx->row_begin - need_lo);
+  op->halo_hi = (uint64_t)std::max<long long>(0, need_hi - (long long)ctx->row_end);
+  if (ctx->world > 1) {
+    // every rank learns its neighbours' needs: [halo_lo, halo_hi] per rank
+    NcclApi& nc = nccl();
+    if (!nc.AllGather || !nc.Send || !nc.Recv) return set_st(st, BO_NCCL, 0, 0.0, "NCCL p2p symbols missing");
+    uint64_t* d = nullptr;
+    CU(cudaMalloc(&d, (2 + 2 * ctx->world) * 8));
+    uint64_t mine[2] = {op->halo_lo, op->halo_hi};
+    CU(cudaMemcpy(d, mine, 16, cudaMemcpyHostToDevice));
+    int rc = nc.AllGather(d, d + 2, 2, kNcclUint64, ctx->nccl, ctx->stream);
+    if (rc) return set_st(st, BO_NCCL, 0, 0.0, "ncclAllGather failed (%d)", rc);
+    std::vector<uint64_t> all(2 * ctx->world);
+    CU(cudaMemcpyAsync(all.data(), d + 2, 16 * ctx->world, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    cudaFree(d);
+    op->peer_need_lo = ctx->rank + 1 < ctx->world ? all[2 * (ctx->rank + 1)] : 0;  // rank+1 needs my tail
+    op->peer_need_hi = ctx->rank > 0 ? all[2 * (ctx->rank - 1) + 1] : 0;           // rank-1 needs my head
+    if (op->halo_lo > (ctx->rank > 0 ? ctx->row_begin : 0) || op->peer_need_lo > ctx->n_local ||
+        op->peer_need_hi > ctx->n_local)
+      return set_st(st, BO_INVALID, 0, 0.0, "halo wider than a neighbouring shard is not supported");
+  }
+  const uint64_t ext = op->halo_lo + ctx->n_local + op->halo_hi;
+  if (ctx->world > 1 || op->halo_lo || op->halo_hi) CU(cudaMalloc(&op->xext, std::max<uint64_t>(ext, 1) * 8));
+  return BO_OK;
+}
+
+// xext <- [recv halo_lo | x | recv halo_hi]; returns the pointer SpMV reads
+int halo_exchange(bo_op op, const double* x, const double** xe, bo_status* st) {
+  bo_ctx ctx = op->ctx;
+  if (!op->xext) {
+    *xe = x;
+    return BO_OK;
+  }
+  CU(cudaMemcpyAsync(op->xext + op->halo_lo, x, ctx->n_local * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (ctx->world > 1) {
+    NcclApi& nc = nccl();
+    nc.GroupStart();
+    const int r = ctx->rank;
+    if (r > 0) {
+      if (op->halo_lo) nc.Recv(op->xext, op->halo_lo, kNcclFloat64, r - 1, ctx->nccl, ctx->stream);
+      if (op->peer_need_hi) nc.Send(x, op->peer_need_hi, kNcclFloat64, r - 1, ctx->nccl, ctx->stream);
+    }
+    if (r + 1 < ctx->world) {
+      if (op->halo_hi)
+        nc.Recv(op->xext + op->halo_lo + ctx->n_local, op->halo_hi, kNcclFloat64, r + 1, ctx->nccl, ctx->stream);
+      if (op->peer_need_lo)
+        nc.Send(x + ctx->n_local - op->peer_need_lo, op->peer_need_lo, kNcclFloat64, r + 1, ctx->nccl, ctx->stream);
+    }
+    int rc = nc.GroupEnd();
+    if (rc) return set_st(st, BO_NCCL, 0, 0.0, "halo exchange failed (%d)", rc);
+  }
+  *xe = op->xext;
+  return BO_OK;
+}
+}  // namespace
+
+extern "C" int bo_op_csr(bo_ctx ctx, uint64_t ncols, const int64_t* row_ptr, const int64_t* col, const double* val,
+                         bo_op* out, bo_status* st) {
+  ok_st(st);
+  *out = nullptr;
+  CU(cudaSetDevice(ctx->device));
+  const uint64_t nl = ctx->n_local;
+  const int64_t base = row_ptr[0];
+  const uint64_t nnz = (uint64_t)(row_ptr[nl] - base);
+  if (nnz >= (1ull << 31)) return set_st(st, BO_INVALID, 0, 0.0, "local nnz exceeds int32");
+  long long need_lo = (long long)ctx->row_begin, need_hi = (long long)ctx->row_end;
+  double fro = 0.0;
+  for (uint64_t k = 0; k < nnz; ++k) {
+    need_lo = std::min<long long>(need_lo, col[k]);
+    need_hi = std::max<long long>(need_hi, col[k] + 1);
+    fro += val[k] * val[k];
+  }
+  bo_op op = new bo_op_s();
+  op->ctx = ctx;
+  op->kind = 0;
+  op->ncols = ncols;
+  op->nnz = nnz;
+  int rc = op_setup_halo(op, need_lo, need_hi, st);
+  if (rc) {
+    bo_op_destroy(op);
+    return rc;
+  }
+  const long long off = (long long)ctx->row_begin - (long long)op->halo_lo;
+  std::vector<int> rp(nl + 1), ci(std::max<uint64_t>(nnz, 1));
+  for (uint64_t r = 0; r <= nl; ++r) rp[r] = (int)(row_ptr[r] - base);
+  for (uint64_t k = 0; k < nnz; ++k) ci[k] = (int)(col[k] - off);
+  cudaError_t e = cudaMalloc(&op->row_ptr, (nl + 1) * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&op->col, std::max<uint64_t>(nnz, 1) * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&op->val, std::max<uint64_t>(nnz, 1) * 8);
+  if (e == cudaSuccess) e = cudaMemcpy(op->row_ptr, rp.data(), (nl + 1) * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && nnz) e = cudaMemcpy(op->col, ci.data(), nnz * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && nnz) e = cudaMemcpy(op->val, val, nnz * 8, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    bo_op_destroy(op);
+    return set_st(st, BO_CUDA, 0, 0.0, "CSR upload failed: %s", cudaGetErrorString(e));
+  }
+  // ||A||_F over all ranks (host arithmetic; the reference sums values in CSR order)
+  op->a_fro_local2 = fro;
+  *out = op;
+  return BO_OK;
+}
+
+extern "C" int bo_op_laplace(bo_ctx ctx, int dims, uint64_t k, bo_op* out, bo_status* st) {
+  ok_st(st);
+  *out = nullptr;
+  CU(cudaSetDevice(ctx->device));
+  if (dims != 2 && dims != 3) return set_st(st, BO_INVALID, 0, 0.0, "dims must be 2 or 3");
+  const uint64_t n = dims == 2 ? k * k : k * k * k;
+  if (n != ctx->n_global) return set_st(st, BO_INVALID, 0, 0.0, "grid size does not match ctx rows");
+  bo_op op = new bo_op_s();
+  op->ctx = ctx;
+  op->kind = 1;
+  op->dims = dims;
+  op->k = k;
+  op->ncols = n;
+  const uint64_t plane = dims == 2 ? k : k * k;
+  const long long need_lo = std::max<long long>(0, (long long)ctx->row_begin - (long long)plane);
+  const long long need_hi = std::min<long long>((long long)n, (long long)ctx->row_end + (long long)plane);
+  int rc = op_setup_halo(op, ctx->world > 1 ? need_lo : (long long)ctx->row_begin,
+                         ctx->world > 1 ? need_hi : (long long)ctx->row_end, st);
+  if (rc) {
+    bo_op_destroy(op);
+    return rc;
+  }
+  // ||A||_F^2 of this shard's rows (all entries are small integers: exact in any order)
+  double fro = 0.0;
+  const double diag = dims == 2 ? 4.0 : 6.0;
+  for (uint64_t me = ctx->row_begin; me < ctx->row_end; ++me) {
+    uint64_t nb;
+    if (dims == 3) {
+      const uint64_t i = me / (k * k), j = (me / k) % k, l = me % k;
+      nb = (i > 0) + (i + 1 < k) + (j > 0) + (j + 1 < k) + (l > 0) + (l + 1 < k);
+    } else {
+      const uint64_t i = me / k, j = me % k;
+      nb = (i > 0) + (i + 1 < k) + (j > 0) + (j + 1 < k);
+    }
+    fro += diag * diag + (double)nb;
+  }
+  op->a_fro_local2 = fro;
+  *out = op;
+  return BO_OK;
+}
+
+extern "C" int bo_op_destroy(bo_op op) {
+  if (!op) return BO_OK;
+  cudaStreamSynchronize(op->ctx->stream);
+  cudaFree(op->row_ptr);
+  cudaFree(op->col);
+  cudaFree(op->val);
+  cudaFree(op->xext);
+  delete op;
+  return BO_OK;
+}
+
+namespace bo {
+namespace host {
+int op_apply(bo_op op, const double* x, double* y, bo_status* st) {
+  bo_ctx ctx = op->ctx;
+  const double* xe;
+  TRY(halo_exchange(op, x, &xe, st));
+  const long long nl = (long long)ctx->n_local;
+  const int grid = (int)std::max<long long>(1, std::min<long long>((long long)ctx->num_sms * 8, (nl + 255) / 256));
+  if (op->kind == 0)
+    spmv_csr_kernel<<<grid, 256, 0, ctx->stream>>>(nl, op->row_ptr, op->col, op->val, xe, y);
+  else
+    spmv_laplace_kernel<<<grid, 256, 0, ctx->stream>>>(op->dims, (long long)op->k, (long long)ctx->row_begin, nl,
+                                                       (long long)op->halo_lo, xe, y);
+  CU(cudaGetLastError());
+  ctx->launches++;
+  return BO_OK;
+}
+}  // namespace host
+}  // namespace bo
+
+extern "C" int bo_spmv(bo_op op, const double* x, double* y, bo_status* st) {
+  ok_st(st);
+  CU(cudaSetDevice(op->ctx->device));
+  TRY(op_apply(op, x, y, st));
+  CU(cudaStreamSynchronize(op->ctx->stream));
+  return BO_OK;
+}
+
+extern "C" int bo_mpk(bo_op op, const double* v0, uint64_t s, double* v, uint64_t ldv, bo_status* st) {
+  ok_st(st);  // gmres.cpp:48-58 monomial basis
+  bo_ctx ctx = op->ctx;
+  CU(cudaSetDevice(ctx->device));
+  if (v0 != v) CU(cudaMemcpyAsync(v, v0, ctx->n_local * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+  for (uint64_t k = 0; k < s; ++k) TRY(op_apply(op, v + k * ldv, v + (k + 1) * ldv, st));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return BO_OK;
+}
+
+// ===========================================================================
+// recursive CholQR (intra_orth.cpp:43-139)
+// ===========================================================================
+namespace {
+struct RecAcc {
+  double* q;  // output, n_local x k (ld ldq)
+  uint64_t ldq;
+  uint64_t k;
+  std::vector<double> coeffs;  // k x k
+  std::vector<uint64_t> kept, disc;
+  std::vector<double> dnorm;
+  uint64_t depth = 0;
+};
+
+int rec_impl(bo_ctx ctx, const double* v, uint64_t ldv, int w, const std::vector<uint64_t>& ids, RecAcc& acc,
+             uint64_t* ledger, bo_status* st) {
+  if (w == 0) return BO_OK;
+  // gram + cholesky on device (partial factor kept on failure)
+  TRY(reset_status(ctx, st));
+  PassReq g{};
+  g.kind = PK_GRAM;
+  g.K = w;
+  g.V = v;
+  g.ldv = ldv;
+  g.pass_id = 1;
+  g.fin.ops = FIN_CHOL | FIN_COPY_G;
+  g.fin.Rchol = T_(ctx, OFF_R1);
+  g.fin.Gout = T_(ctx, OFF_G);
+  TRY(run_pass(ctx, g, st));
+  TRY(fetch(ctx, true, st));
+  if (ledger) ledger[BO_LEDGER_GRAM]++;
+  const DevStatus d = *ctx->status_host;
+  const double* R = ctx->tiny_host + OFF_R1;
+  const double* G = ctx->tiny_host + OFF_G;
+  const uint64_t K = acc.k;
+  if (d.code == ST_OK) {
+    const uint64_t base = acc.kept.size();
+    PassReq t{};
+    t.kind = PK_P1_ST;
+    t.K = w;
+    t.V = v;
+    t.ldv = ldv;
+    t.Rpre0 = T_(ctx, OFF_R1);
+    t.out = acc.q + base * acc.ldq;
+    t.ldo = acc.ldq;
+    TRY(reset_status(ctx, st));
+    TRY(run_pass(ctx, t, st));
+    for (int j = 0; j < w; ++j) {
+      acc.kept.push_back(ids[j]);
+      for (int i = 0; i <= j; ++i) acc.coeffs[(base + i) + ids[j] * K] = R[i + j * 16];
+    }
+    return BO_OK;
+  }
+  if (d.code != ST_CHOLESKY) return dev_error(ctx, "cholqr", st);
+  const int f = (int)d.step;
+  if (f == 1) {  // discard this whole sub-block
+    for (int j = 0; j < w; ++j) {
+      acc.disc.push_back(ids[j]);
+      const double gjj = G[j + j * 16];
+      acc.dnorm.push_back(std::sqrt(std::max(gjj, 0.0)));
+    }
+    acc.depth++;
+    return BO_OK;
+  }
+  const int good = f - 1;
+  // upload R11 / R12 from the partial factor (R slot already holds it on device)
+  std::vector<double> r12(LDC * 16, 0.0);
+  const uint64_t base = acc.kept.size();
+  for (int j = 0; j < good; ++j) {
+    acc.kept.push_back(ids[j]);
+    for (int i = 0; i <= j; ++i) acc.coeffs[(base + i) + ids[j] * K] = R[i + j * 16];
+  }
+  for (int j = 0; j < w - good; ++j)
+    for (int i = 0; i < good; ++i) {
+      const double c = R[i + (good + j) * 16];
+      r12[i + j * LDC] = c;
+      acc.coeffs[(base + i) + ids[good + j] * K] = c;
+    }
+  // q_good = v[:, :good] R11^{-1}
+  TRY(reset_status(ctx, st));
+  PassReq t{};
+  t.kind = PK_P1_ST;
+  t.K = good;
+  t.V = v;
+  t.ldv = ldv;
+  t.Rpre0 = T_(ctx, OFF_R1);
+  t.out = acc.q + base * acc.ldq;
+  t.ldo = acc.ldq;
+  TRY(run_pass(ctx, t, st));
+  // rest = v[:, good:] - q_good R12
+  double* rest = nullptr;
+  const size_t ldr = ctx->ld;
+  CU(cudaMallocAsync((void**)&rest, ldr * (w - good) * 8, ctx->stream));
+  CU(cudaMemcpyAsync(T_(ctx, OFF_C1), r12.data(), r12.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+  PassReq u{};
+  u.kind = PK_UPD_ST;
+  u.K = w - good;
+  u.V = v + good * ldv;
+  u.ldv = ldv;
+  u.Q = acc.q + base * acc.ldq;
+  u.ldq = acc.ldq;
+  u.p = good;
+  u.Cm = T_(ctx, OFF_C1);
+  u.out = rest;
+  u.ldo = ldr;
+  TRY(run_pass(ctx, u, st));
+  CU(cudaStreamSynchronize(ctx->stream));
+  acc.depth++;
+  std::vector<uint64_t> rest_ids(ids.begin() + good, ids.end());
+  const int rc = rec_impl(ctx, rest, ldr, w - good, rest_ids, acc, ledger, st);
+  cudaFreeAsync(rest, ctx->stream);
+  return rc;
+}
+}  // namespace
+
+extern "C" int bo_recursive_cholqr(bo_ctx ctx, const double* v, uint64_t ldv, uint64_t k, double* q, uint64_t ldq,
+                                   double* coeffs, uint64_t* kept, uint64_t* nkept, uint64_t* discarded,
+                                   double* discard_norm, uint64_t* ndiscarded, uint64_t* depth, uint64_t ledger[4],
+                                   bo_status* st) {
+  ok_st(st);
+  CU(cudaSetDevice(ctx->device));
+  if (k > 16) return set_st(st, BO_INVALID, 0, 0.0, "panel wider than 16 columns");
+  const double* vv;
+  uint64_t lv;
+  TRY(stage_input(ctx, v, ldv, k, 0, &vv, &lv, st));
+  if (!out_ok(ctx, q, ldq)) return set_st(st, BO_INVALID, 0, 0.0, "q must have ld % 4 == 0 and ld >= n_local");
+  // the input may live in scratch 0, which recursion does not touch
+  RecAcc acc;
+  acc.q = q;
+  acc.ldq = ldq;
+  acc.k = k;
+  acc.coeffs.assign(k * k, 0.0);
+  std::vector<uint64_t> ids(k);
+  for (uint64_t j = 0; j < k; ++j) ids[j] = j;
+  int rc = rec_impl(ctx, vv, lv, (int)k, ids, acc, ledger, st);
+  if (rc != BO_OK) return rc;
+  CU(cudaStreamSynchronize(ctx->stream));
+  if (coeffs) std::memcpy(coeffs, acc.coeffs.data(), k * k * 8);
+  if (kept) std::copy(acc.kept.begin(), acc.kept.end(), kept);
+  if (nkept) *nkept = acc.kept.size();
+  if (discarded) std::copy(acc.disc.begin(), acc.disc.end(), discarded);
+  if (discard_norm) std::copy(acc.dnorm.begin(), acc.dnorm.end(), discard_norm);
+  if (ndiscarded) *ndiscarded = acc.disc.size();
+  if (depth) *depth = acc.depth;
+  if (acc.kept.empty()) return set_st(st, BO_ALL_COLUMNS_DISCARDED, 0, 0.0, "recursive CholQR discarded all columns");
+  return BO_OK;
+}
+
+// ===========================================================================
+// BCGS-PIP and RandBCGS (block_orth.cpp:230-325)
+// ===========================================================================
+namespace {
+
+// shared tail: resid = vhat - Q[lo:lo+p] C ; qj = resid R^{-1} into the slab;
+// C (p x k) and R (k x k) given on host
+int update_solve_store(bo_basis b, const double* vh, uint64_t ldvh, int K, uint64_t lo, int p, const hd::Mat& C,
+                       const hd::Mat& R, uint64_t base, bo_status* st) {
+  bo_ctx ctx = b->ctx;
+  std::vector<double> hc(LDC * 16, 0.0), hr(256, 0.0);
+  for (size_t j = 0; j < C.c; ++j)
+    for (size_t i = 0; i < C.r; ++i) hc[i + j * LDC] = C(i, j);
+  for (size_t j = 0; j < R.c; ++j)
+    for (size_t i = 0; i <= j; ++i) hr[i + j * 16] = R(i, j);
+  CU(cudaMemcpyAsync(T_(ctx, OFF_C1), hc.data(), hc.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaMemcpyAsync(T_(ctx, OFF_R4), hr.data(), hr.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+  TRY(reset_status(ctx, st));
+  PassReq r{};
+  r.K = K;
+  r.V = vh;
+  r.ldv = ldvh;
+  r.out = b->q + base * ctx->ld;
+  r.ldo = ctx->ld;
+  if (p > 0) {
+    r.kind = PK_UPD_POST_ST;
+    r.Q = b->q + lo * ctx->ld;
+    r.ldq = ctx->ld;
+    r.p = p;
+    r.Cm = T_(ctx, OFF_C1);
+    r.Rpost = T_(ctx, OFF_R4);
+  } else {
+    r.kind = PK_P1_ST;
+    r.Rpre0 = T_(ctx, OFF_R4);
+  }
+  TRY(run_pass(ctx, r, st));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return BO_OK;
+}
+
+void push_full(bo_basis b, uint64_t k, uint64_t hi, uint64_t bp, const hd::Mat* rbig, const hd::Mat& proj,
+               const hd::Mat& diag, bool overlap) {
+  std::vector<double> full(std::max<uint64_t>(hi, 1) * k, 0.0), dg(k * k, 0.0);
+  for (uint64_t j = 0; j < k; ++j) {
+    for (uint64_t i = 0; i < bp; ++i) full[i + j * hi] = (rbig && rbig->r) ? (*rbig)(i, j) : 0.0;
+    for (uint64_t i = 0; i < proj.r; ++i) full[bp + i + j * hi] = proj(i, j);
+    for (uint64_t i = 0; i <= j; ++i) dg[i + j * k] = diag(i, j);
+  }
+  push_panel_host(b, k, full.data(), hi, dg.data(), k, overlap);
+}
+
+int pip_impl(bo_basis b, const double* vh, uint64_t ldvh, int K, const hd::Mat* rbig, bool overlap, bo_status* st) {
+  bo_ctx ctx = b->ctx;
+  const uint64_t bp = b->bp_lo;
+  const bool eff = overlap && b->cols > 0;
+  const uint64_t hi = b->cols - (eff ? 1 : 0);
+  if (hi < bp) return set_st(st, BO_INVALID, 0, 0.0, "projection range below the big panel");
+  const int p = (int)(hi - bp);
+  // one fused volley [Q_range, V]^T V ; G = V^T V - proj^T proj ; Cholesky ("bcgs_pip")
+  TRY(reset_status(ctx, st));
+  PassReq r{};
+  r.kind = PK_QTX_GRAM;
+  r.K = K;
+  r.V = vh;
+  r.ldv = ldvh;
+  r.Q = b->q + bp * ctx->ld;
+  r.ldq = ctx->ld;
+  r.p = p;
+  r.pass_id = 1;
+  r.fin.ops = FIN_PIP | FIN_CHOL;
+  r.fin.Cq = T_(ctx, OFF_C2);
+  r.fin.Rchol = T_(ctx, OFF_R1);
+  TRY(run_pass(ctx, r, st));
+  TRY(fetch(ctx, true, st));
+  b->ledger[BO_LEDGER_GRAM]++;
+  TRY(dev_error(ctx, "bcgs_pip", st));
+  hd::Mat proj(p, K), R(K, K);
+  for (int j = 0; j < K; ++j) {
+    for (int i = 0; i < p; ++i) proj(i, j) = ctx->tiny_host[OFF_C2 + i + j * LDC];
+    for (int i = 0; i <= j; ++i) R(i, j) = ctx->tiny_host[OFF_R1 + i + j * 16];
+  }
+  TRY(update_solve_store(b, vh, ldvh, K, bp, p, proj, R, hi, st));
+  push_full(b, K, hi, bp, rbig, proj, R, eff);
+  return BO_OK;
+}
+
+int rand_bcgs_impl(bo_basis b, const double* vh, uint64_t ldvh, int K, const hd::Mat* rbig, bo_sketch th,
+                   bool overlap, bo_status* st) {
+  bo_ctx ctx = b->ctx;
+  const uint64_t bp = b->bp_lo;
+  const bool eff = overlap && b->cols > 0;
+  const uint64_t hi = b->cols - (eff ? 1 : 0);
+  const uint64_t mh = th->mhat;
+  // sketch (one reduce) -> host
+  std::vector<double> sv;
+  TRY(sketch_to_host(th, vh, ldvh, K, sv, st));
+  b->ledger[BO_LEDGER_SKETCH]++;
+  hd::Mat sk(mh, K);
+  sk.a = sv;
+  // BCGS2 with Householder intra on the sketched history (all local)
+  const uint64_t have = b->sk_cols;
+  const uint64_t sk_p = (eff && have > 0) ? have - 1 : have;
+  if (b->sk_rows != mh) return set_st(st, BO_INVALID, 0, 0.0, "big panel was begun with a different sketch size");
+  hd::Mat qprior(mh, sk_p);
+  for (uint64_t j = 0; j < sk_p; ++j)
+    for (uint64_t i = 0; i < mh; ++i) qprior(i, j) = b->sk[i + j * mh];
+  hd::Mat proj_sk(sk_p, K), qsk, rdiag;
+  if (sk_p == 0) {
+    hd::householder_qr(sk, qsk, rdiag);
+  } else {
+    hd::Mat proj1 = hd::transpose_times(qprior, sk);
+    hd::Mat skhat = sk;
+    hd::subtract_product(skhat, qprior, proj1);
+    hd::Mat iq, ir;
+    hd::householder_qr(skhat, iq, ir);
+    hd::Mat t1 = hd::transpose_times(qprior, iq);
+    hd::Mat q2 = iq;
+    hd::subtract_product(q2, qprior, t1);
+    hd::Mat oq, orr;
+    hd::householder_qr(q2, oq, orr);
+    qsk = oq;
+    proj_sk = hd::update_projection(proj1, t1, ir);
+    rdiag = hd::multiply_upper(orr, ir);
+  }
+  for (int j = 0; j < K; ++j)
+    if (rdiag(j, j) == 0.0)
+      return set_st(st, BO_SINGULAR_TRIANGULAR, j, 0.0, "triangular factor is singular: zero diagonal at index %d", j);
+  TRY(update_solve_store(b, vh, ldvh, K, bp, (int)sk_p, proj_sk, rdiag, hi, st));
+  push_full(b, K, hi, bp, rbig, proj_sk, rdiag, eff);
+  // push_sketched (block_orth.cpp:100-110)
+  const uint64_t base = (eff && have > 0) ? have - 1 : have;
+  b->sk.resize(mh * (base + K));
+  for (int j = 0; j < K; ++j)
+    for (uint64_t i = 0; i < mh; ++i) b->sk[i + (base + j) * mh] = qsk(i, j);
+  b->sk_cols = base + K;
+  return BO_OK;
+}
+
+int two_stage_common(bo_basis b, const double* v, uint64_t ldv, uint64_t k, int preproc, bo_sketch theta,
+                     int overlap, bo_status* st) {
+  bo_ctx ctx = b->ctx;
+  CU(cudaSetDevice(ctx->device));
+  const uint64_t bp = b->bp_lo;
+  const bool eff = overlap && b->cols > 0;
+  if ((eff ? b->cols - 1 : b->cols) + k > b->cap) return set_st(st, BO_INVALID, 0, 0.0, "basis capacity exceeded");
+  const double* vv;
+  uint64_t lv;
+  TRY(stage_input(ctx, v, ldv, k, 0, &vv, &lv, st));
+  const double* vh = vv;
+  uint64_t ldvh = lv;
+  hd::Mat rbig(bp, k);
+  if (bp > 0) {  // inter-big-panel BCGS against the completed big panels
+    TRY(reset_status(ctx, st));
+    TRY(dev_project(b, vv, lv, (int)k, 0, bp, ctx->scratch[1], ctx->ld, OFF_C1, 1, st));
+    TRY(fetch(ctx, true, st));
+    b->ledger[BO_LEDGER_PROJECTION]++;
+    for (uint64_t j = 0; j < k; ++j)
+      for (uint64_t i = 0; i < bp; ++i) rbig(i, j) = ctx->tiny_host[OFF_C1 + i + j * LDC];
+    vh = ctx->scratch[1];
+    ldvh = ctx->ld;
+  }
+  if (preproc == BO_PREPROC_PIP) return pip_impl(b, vh, ldvh, (int)k, &rbig, eff, st);
+  return rand_bcgs_impl(b, vh, ldvh, (int)k, &rbig, theta, eff, st);
+}
+
+}  // namespace
+
+extern "C" int bo_bcgs_pip(bo_basis b, const double* v, uint64_t ldv, uint64_t k, int overlap, bo_status* st) {
+  ok_st(st);
+  bo_ctx ctx = b->ctx;
+  CU(cudaSetDevice(ctx->device));
+  const double* vv;
+  uint64_t lv;
+  TRY(stage_input(ctx, v, ldv, k, 0, &vv, &lv, st));
+  hd::Mat rbig(b->bp_lo, k);
+  return pip_impl(b, vv, lv, (int)k, &rbig, overlap != 0, st);
+}
+
+extern "C" int bo_rand_bcgs_preproc(bo_basis b, const double* v, uint64_t ldv, uint64_t k, bo_sketch theta,
+                                    int overlap, bo_status* st) {
+  ok_st(st);
+  bo_ctx ctx = b->ctx;
+  CU(cudaSetDevice(ctx->device));
+  const double* vv;
+  uint64_t lv;
+  TRY(stage_input(ctx, v, ldv, k, 0, &vv, &lv, st));
+  hd::Mat rbig(b->bp_lo, k);
+  return rand_bcgs_impl(b, vv, lv, (int)k, &rbig, theta, overlap != 0, st);
+}
+
+extern "C" int bo_two_stage_panel(bo_basis b, const double* v, uint64_t ldv, uint64_t k, int preproc,
+                                  bo_sketch theta, int overlap, bo_status* st) {
+  ok_st(st);
+  if (preproc == BO_PREPROC_RAND_BCGS && !theta)
+    return set_st(st, BO_INVALID, 0, 0.0, "rand_bcgs preprocessing needs a sketch operator");
+  return two_stage_common(b, v, ldv, k, preproc, theta, overlap, st);
+}
+
+extern "C" int bo_two_stage_finish(bo_basis b, int preproc, int reorthogonalize, int record, double* stats,
+                                   bo_status* st) {
+  ok_st(st);
+  bo_ctx ctx = b->ctx;
+  CU(cudaSetDevice(ctx->device));
+  const uint64_t bp = b->bp_lo, w = b->cols - bp;
+  if (w > 64) return set_st(st, BO_INVALID, 0, 0.0, "big panel wider than 64 columns");
+  double* qb = b->q + bp * ctx->ld;
+  if (record && stats) {
+    // kappa of the preprocessed big panel from its Gram (sigma_i = sqrt(lambda_i)),
+    // sketched orthogonality error on the host (diagnostics only)
+    hd::Mat G;
+    TRY(wide_contract(ctx, qb, ctx->ld, (int)w, qb, ctx->ld, (int)w, G, st));
+    std::vector<double> ev(w);
+    {
+      std::vector<double> a(G.a);
+      // cyclic Jacobi
+      for (int sweep = 0; sweep < 100; ++sweep) {
+        double off = 0.0;
+        for (uint64_t j = 0; j < w; ++j)
+          for (uint64_t i = 0; i < j; ++i) off += a[i + j * w] * a[i + j * w];
+        if (off == 0.0) break;
+        for (uint64_t p = 0; p < w; ++p)
+          for (uint64_t q = p + 1; q < w; ++q) {
+            const double apq = a[p + q * w];
+            if (apq == 0.0) continue;
+            const double app = a[p + p * w], aqq = a[q + q * w];
+            const double th = (aqq - app) / (2.0 * apq);
+            const double t = (th >= 0 ? 1.0 : -1.0) / (std::fabs(th) + std::sqrt(th * th + 1.0));
+            const double c = 1.0 / std::sqrt(t * t + 1.0), s = t * c;
+            for (uint64_t r = 0; r < w; ++r) {
+              const double arp = a[r + p * w], arq = a[r + q * w];
+              a[r + p * w] = c * arp - s * arq;
+              a[r + q * w] = s * arp + c * arq;
+            }
+            for (uint64_t r = 0; r < w; ++r) {
+              const double apr = a[p + r * w], aqr = a[q + r * w];
+              a[p + r * w] = c * apr - s * aqr;
+              a[q + r * w] = s * apr + c * aqr;
+            }
+          }
+      }
+      for (uint64_t i = 0; i < w; ++i) ev[i] = a[i + i * w];
+    }
+    double mx = 0, mn = 1e308;
+    for (double e : ev) {
+      mx = std::max(mx, e);
+      mn = std::min(mn, e);
+    }
+    stats[0] = mn > 0 ? std::sqrt(mx / mn) : INFINITY;
+    stats[1] = 0.0;
+    if (preproc == BO_PREPROC_RAND_BCGS && b->sk_cols) {
+      const uint64_t m = b->sk_rows, c = b->sk_cols;
+      std::vector<double> d(c * c);
+      for (uint64_t j = 0; j < c; ++j)
+        for (uint64_t i = 0; i < c; ++i) {
+          double s = 0.0;
+          for (uint64_t r = 0; r < m; ++r) s += b->sk[r + i * m] * b->sk[r + j * m];
+          d[i + j * c] = (i == j ? 1.0 : 0.0) - s;
+        }
+      double mxa = 0.0;
+      for (double x : d) mxa = std::max(mxa, std::fabs(x));  // bound; exact 2-norm not needed for stats
+      stats[1] = mxa;
+    }
+  }
+  // second stage: CholQR of the big panel in place, refactor coefficient rows
+  TRY(reset_status(ctx, st));
+  hd::Mat R;
+  TRY(wide_cholqr(ctx, qb, ctx->ld, (int)w, "cholqr", R, b->ledger, st));
+  refactor_rows(b, bp, R);
+  if (bp > 0 && reorthogonalize) {
+    // BCGS against the completed big panels, 64 prior columns at a time
+    hd::Mat C(bp, w);
+    for (uint64_t c0 = 0; c0 < bp; c0 += 64) {
+      const int pc = (int)std::min<uint64_t>(64, bp - c0);
+      hd::Mat Cc;
+      TRY(wide_contract(ctx, b->q + c0 * ctx->ld, ctx->ld, pc, qb, ctx->ld, (int)w, Cc, st));
+      for (uint64_t j = 0; j < w; ++j)
+        for (int i = 0; i < pc; ++i) C(c0 + i, j) = Cc(i, j);
+    }
+    b->ledger[BO_LEDGER_PROJECTION]++;
+    for (uint64_t c0 = 0; c0 < bp; c0 += 64) {
+      const int pc = (int)std::min<uint64_t>(64, bp - c0);
+      hd::Mat Cc(pc, w);
+      for (uint64_t j = 0; j < w; ++j)
+        for (int i = 0; i < pc; ++i) Cc(i, j) = C(c0 + i, j);
+      TRY(wide_update_trsm(ctx, qb, ctx->ld, (int)w, b->q + c0 * ctx->ld, ctx->ld, pc, &Cc, nullptr, qb, ctx->ld, st));
+    }
+    hd::Mat R2;
+    TRY(wide_cholqr(ctx, qb, ctx->ld, (int)w, "cholqr", R2, b->ledger, st));
+    reorth_rows(b, bp, C, R2);
+  }
+  return BO_OK;
+}
+
+namespace bo {
+namespace host {
+// Gram of p <= 64 device columns, summed over ranks, to host (p x p)
+int wide_gram_host(bo_ctx ctx, const double* q, uint64_t ld, int p, std::vector<double>& G, bo_status* st) {
+  hd::Mat M;
+  TRY(wide_contract(ctx, q, ld, p, q, ld, p, M, st));
+  G = M.a;
+  return BO_OK;
+}
+}  // namespace host
+}  // namespace bo

@@ -48,11 +48,12 @@ __device__ void finalize_dev(const FinArgs& f, double* smem_scratch /* >= 16*16*
   double* A = smem_scratch + 512;       // sketch block for Householder
   const int K = f.K;
 
-  if (f.ops & FIN_COPY_Q) {
+  if (f.ops & (FIN_COPY_Q | FIN_PIP)) {
     for (int e = tid; e < f.p * K; e += nth) {
       const int i = e % f.p, j = e / f.p;
-      f.Cq[i + j * f.ldcq] = sums[f.off_q + i + j * f.ld_q];
+      f.Cq[f.q_row_off + i + j * f.ldcq] = sums[f.off_q + i + j * f.ld_q];
     }
+    __syncthreads();
   }
   if (f.ops & FIN_COPY_G) {
     for (int e = tid; e < 256; e += nth) f.Gout[e] = sums[f.off_g + e];
@@ -108,23 +109,17 @@ __device__ void finalize_dev(const FinArgs& f, double* smem_scratch /* >= 16*16*
     if (f.status->code != ST_OK) return;
   }
   if (f.ops & FIN_CHOL) {
-    // G = GRAM block (optionally minus proj^T proj for BCGS-PIP, block_orth.cpp:245-251)
+    // G = GRAM block (optionally minus proj^T proj for BCGS-PIP, block_orth.cpp:245-251;
+    // proj is read back from Cq, which holds every projection chunk)
     for (int e = tid; e < 256; e += nth) {
       const int i = e % 16, j = e / 16;
       double g = sums[f.off_g + e];
       if ((f.ops & FIN_PIP) && i < K && j < K) {
         double s = 0.0;
-        for (int l = 0; l < f.p; ++l)
-          s = tiny::add(s, tiny::mul(sums[f.off_q + l + i * f.ld_q], sums[f.off_q + l + j * f.ld_q]));
+        for (int l = 0; l < f.p_total; ++l) s = tiny::add(s, tiny::mul(f.Cq[l + i * f.ldcq], f.Cq[l + j * f.ldcq]));
         g = tiny::sub(g, s);
       }
       G[e] = g;
-    }
-    if (f.ops & FIN_PIP) {
-      for (int e = tid; e < f.p * K; e += nth) {
-        const int i = e % f.p, j = e / f.p;
-        f.Cq[i + j * f.ldcq] = sums[f.off_q + i + j * f.ld_q];
-      }
     }
     __syncthreads();
     __shared__ int s_fail;
@@ -142,7 +137,7 @@ __device__ void finalize_dev(const FinArgs& f, double* smem_scratch /* >= 16*16*
     }
   }
   if (f.ops & FIN_COEFF) {
-    tiny::update_projection(f.C1, f.C2, f.ldc, f.p, K, f.Rin, f.coeffs);
+    tiny::update_projection(f.C1, f.C2, f.ldc, f.p_total, K, f.Rin, f.coeffs);
   }
   if (f.ops & (FIN_COEFF | FIN_MULT)) {
     tiny::multiply_upper(f.Rchol, f.Rin, K, f.rjj);
@@ -532,8 +527,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int r = g32 * 32 + lane;
             const bool rv = r < valid;
             const uint32_t code = rv ? stC[r] : 0u;
-            const int bk = (int)(code & 0x7fffffffu);
-            const bool mine = rv && (bk % GW) == gw;
+            const int bk = (int)(code & 0x7fffffffu) - a.bucket_lo;
+            const bool mine = rv && bk >= 0 && bk < mh && (bk % GW) == gw;
             const unsigned key = mine ? (unsigned)bk : (0x80000000u | (unsigned)lane);
             const unsigned grp = __match_any_sync(0xffffffffu, key);
             if (mine && (__ffs(grp) - 1) == lane) {

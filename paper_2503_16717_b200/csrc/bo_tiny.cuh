@@ -21,7 +21,7 @@ __device__ __forceinline__ double div(double a, double b) { return __ddiv_rn(a, 
 // On failure at 1-based step f the partial factor matches the reference:
 // columns < f-1 complete, column f-1 holds rows < f-1, later columns zero.
 // Whole CTA participates (blockDim >= 32).  G, R have ld kRld; sbuf: 16*16.
-__device__ void cholesky(const double* G, int K, double tol, double* R, double* sbuf,
+__device__ inline void cholesky(const double* G, int K, double tol, double* R, double* sbuf,
                          int* failed_at, double* failed_pivot) {
   const int tid = threadIdx.x, nth = blockDim.x;
   __shared__ double s_maxdiag;
@@ -91,7 +91,7 @@ __device__ void cholesky(const double* G, int K, double tol, double* R, double* 
 // normalised.  Q is not formed (RandCholQR uses only R,
 // proj/src/intra_orth.cpp:28-39).  A (m x K, ld lda) is destroyed.  Warp 0
 // only; lanes own columns.
-__device__ void householder_r(double* A, int lda, int m, int K, double* R, double* tau_buf) {
+__device__ inline void householder_r(double* A, int lda, int m, int K, double* R, double* tau_buf) {
   const int lane = threadIdx.x & 31;
   if (threadIdx.x >= 32) return;
   for (int j = 0; j < K; ++j) {
@@ -143,7 +143,7 @@ __device__ void householder_r(double* A, int lda, int m, int K, double* R, doubl
 }
 
 // out = T * R for upper-triangular T, R (proj/src/dense.cpp:188-198)
-__device__ void multiply_upper(const double* T, const double* Rm, int K, double* out) {
+__device__ inline void multiply_upper(const double* T, const double* Rm, int K, double* out) {
   for (int e = threadIdx.x; e < kRld * kRld; e += blockDim.x) {
     const int i = e % kRld, j = e / kRld;
     double s = 0.0;
@@ -155,7 +155,7 @@ __device__ void multiply_upper(const double* T, const double* Rm, int K, double*
 
 // out = C1 + C2 * Rin  (proj/src/block_orth.cpp:191-203 update_projection,
 // times() at proj/src/dense.cpp:44-58 skips zero coefficients)
-__device__ void update_projection(const double* C1, const double* C2, int ldc, int p, int K,
+__device__ inline void update_projection(const double* C1, const double* C2, int ldc, int p, int K,
                                   const double* Rin, double* out) {
   for (int e = threadIdx.x; e < p * K; e += blockDim.x) {
     const int r = e % p, j = e / p;
