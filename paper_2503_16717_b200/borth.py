@@ -164,6 +164,10 @@ class Context:
             row_begin, row_end = 0, n
         self.n, self.rank, self.world = n, rank, world
         self.row_begin, self.row_end = row_begin, row_end
+        if not torch.cuda.is_available():
+            # let the library report it: the path has no CPU fallback
+            h = C.c_void_p()
+            _call(self.lib.bo_ctx_create, device, rank, world, None, n, row_begin, row_end, None, C.byref(h))
         self.device = torch.device("cuda", device)
         torch.cuda.set_device(self.device)
         # the library runs on this (non-default) stream; torch work that feeds
