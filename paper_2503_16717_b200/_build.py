@@ -54,6 +54,20 @@ def build_cuda(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+def build_examples() -> None:
+    """C++ host program over the C ABI (examples/cpp_gmres.cpp)."""
+    ex = PKG.parent / "examples"
+    src = ex / "cpp_gmres.cpp"
+    out = ex / "cpp_gmres"
+    if not src.exists() or not _stale(out, [src, INCLUDE / "blkorth_gpu.hpp", INCLUDE / "bo_cuda.h", LIB]):
+        return
+    cuda = Path(_nvcc()).resolve().parents[1]
+    cmd = ["g++", "-std=c++17", "-O2", f"-I{INCLUDE}", f"-I{cuda / 'include'}", str(src), "-o", str(out),
+           f"-L{PKG}", "-lbo_cuda", f"-Wl,-rpath,{PKG}", f"-L{cuda / 'lib64'}", "-lcudart",
+           f"-Wl,-rpath,{cuda / 'lib64'}"]
+    subprocess.run(cmd, check=True)
+
+
 def build_oracle(verbose: bool = False) -> None:
     """Build the parity checkers (oracle/ restatement and, when the reference
     sources are present, oracle/_ref).  Test infrastructure only."""
@@ -67,4 +81,5 @@ def build_oracle(verbose: bool = False) -> None:
 
 if __name__ == "__main__":
     build_cuda(verbose=True)
+    build_examples()
     build_oracle(verbose=True)
