@@ -156,15 +156,15 @@ PassFn pass_fn(int kind) {
   return nullptr;
 }
 // triangular-solve passes specialised on the panel width (s = 5, 10, 15)
-template <int KC>
+template <int KC, int T>
 PassFn pass_fn_kc(int kind) {
   constexpr int NT = KC <= 8 ? 1 : 2;
   switch (kind) {
-#define X(nm, a, b, c, d, e, f, g)                              \
-  case PK_##nm:                                                 \
-    if constexpr (a > 0 || c > 0)                               \
-      return pass_kernel<NT, 128, a, b, c, d, e, f, g, false, KC>; \
-    else                                                        \
+#define X(nm, a, b, c, d, e, f, g)                             \
+  case PK_##nm:                                                \
+    if constexpr (a > 0 || c > 0)                              \
+      return pass_kernel<NT, T, a, b, c, d, e, f, g, false, KC>; \
+    else                                                       \
       return nullptr;
     BO_PASS_KINDS(X)
 #undef X
@@ -176,11 +176,17 @@ PassFn get_pass_fn(int nt, int T, int kind, bool exact, int K) {
     return nt == 1 ? (PassFn)pass_kernel<1, 64, 1, false, 0, false, false, SK_NONE, true, true>
                    : (PassFn)pass_kernel<2, 64, 1, false, 0, false, false, SK_NONE, true, true>;
   const KindInfo& ki = kKindInfo[kind];
-  if (T == 128 && (ki.npre > 0 || ki.npost > 0)) {
+  if (ki.npre > 0 || ki.npost > 0) {
     PassFn f = nullptr;
-    if (K == 6) f = pass_fn_kc<6>(kind);
-    if (K == 11) f = pass_fn_kc<11>(kind);
-    if (K == 16) f = pass_fn_kc<16>(kind);
+    if (T == 128) {
+      if (K == 6) f = pass_fn_kc<6, 128>(kind);
+      if (K == 11) f = pass_fn_kc<11, 128>(kind);
+      if (K == 16) f = pass_fn_kc<16, 128>(kind);
+    } else {
+      if (K == 6) f = pass_fn_kc<6, 64>(kind);
+      if (K == 11) f = pass_fn_kc<11, 64>(kind);
+      if (K == 16) f = pass_fn_kc<16, 64>(kind);
+    }
     if (f) return f;
   }
   if (nt == 1) return T == 128 ? pass_fn<1, 128>(kind) : pass_fn<1, 64>(kind);
@@ -248,7 +254,7 @@ int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st) {
                                         ki.sk == SK_COUNT, tt);
     const size_t stage = (size_t)SL.stage * 8;
     const bool xt = ki.npre > 0 || ki.upd || ki.npost > 0;
-    const size_t fixed = (xt ? 2 * (size_t)r.K * S * 8 : 0) + (3 * 256 + 48) * 8 +
+    const size_t fixed = (xt ? 2 * (size_t)nt * 8 * S * 8 : 0) + (3 * 256 + 48) * 8 +
                          (ki.sk == SK_COUNT ? (size_t)mh * r.K * 8 : 0) + 2 * kMaxStages * 8;
     const size_t need_red = (size_t)kConsumerWarps * dm_len * 8;
     const size_t need_fin = (512 + (size_t)std::max(mh, 1) * 16 + 64) * 8;
@@ -257,8 +263,8 @@ int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st) {
     if (ns < 1) continue;
     const size_t r0 = round_up(std::max({(size_t)ns * stage, need_red, need_fin}), 128);
     if (r0 + fixed > avail) continue;
-    // TMA moves one box per operand per tile: prefer the larger tile once two
-    // stages fit (double buffering), else the deeper ring.
+    // Prefer the 128-row tile (fewer barriers per byte; measured faster at
+    // every pass shape) whenever it double-buffers; else the deeper 64-row ring.
     const bool better = T == 0 || (ns >= 2 && NS < 2);
     if (better) {
       T = tt;

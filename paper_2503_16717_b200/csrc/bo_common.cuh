@@ -22,9 +22,10 @@ __host__ __device__ inline StageLayout stage_layout(int K, int ncolQ, int ncolT,
   const int S = T + 4;
   StageLayout L;
   L.offV = 0;
-  L.offQ = ru16(K * S);
-  L.offT = L.offQ + ru16(ncolQ * S);
-  L.offC = L.offT + ru16(ncolT * S);
+  // operand blocks hold a multiple of 8 columns (zero padding for the MMA tiles)
+  L.offQ = ru16(((K + 7) & ~7) * S);
+  L.offT = L.offQ + ru16(((ncolQ + 7) & ~7) * S);
+  L.offC = L.offT + ru16(((ncolT + 7) & ~7) * S);
   L.stage = L.offC + (count ? ru16(T / 2) : 0);
   return L;
 }

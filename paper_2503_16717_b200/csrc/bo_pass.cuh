@@ -22,6 +22,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "bo_common.cuh"
 #include "bo_ptx.cuh"
 #include "bo_tiny.cuh"
@@ -217,9 +219,12 @@ __device__ __forceinline__ void row_trsm_n(double (&x)[NR][kMaxK], const double*
 //                 Theta) + a 1-D bulk copy of the Count codes, mbarrier ring.
 //   warps 0..7    consumers.  Without a pre-TRSM they form one group that runs
 //                 U -> A' -> S -> R on each tile.  With a pre-TRSM (NPRE > 0)
-//                 they split: warps 0-3 solve rows (A) into a double-buffered
-//                 X tile while warps 4-7 run U/S/R on the previous tile, handed
-//                 over with named-barrier arrive/sync pairs.
+//                 warps 0-1 solve rows (A) into a double-buffered X tile while
+//                 warps 2-7 run U/S/R on the previous tile, handed over with
+//                 named-barrier arrive/sync pairs.
+// Every staged operand block is zero-padded to a multiple of 8 columns and
+// TMA zero-fills rows past the matrix, so the tensor-core loops need no masks;
+// the number of 8-column tiles is dispatched to a compile-time constant.
 template <int NT, int T, int NPRE, bool UPD, int NPOST, bool QTX, bool GRAM, int SK, bool STORE, bool EXACT,
           int KC = 0>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -231,8 +236,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int GAW = SPLIT ? 2 : 0;       // row-solve warps (2 rows per thread)
   constexpr int GW = NW - GAW;             // warps of the U/S/R group
   constexpr int GT = GW * 32;
-  constexpr int GBAR = SPLIT ? 6 : 1;  // named barrier of the U/S/R group
+  constexpr int GBAR = SPLIT ? 6 : 1;      // named barrier of the U/S/R group
   constexpr bool XT = (NPRE > 0) || UPD || (NPOST > 0);  // X lives in the X tile
+  constexpr int KP = NT * 8;               // padded panel width
   constexpr int MQT = kMaxPTile / 8;
   constexpr int MST = 4;
   static_assert(!(QTX && UPD), "a pass either projects or updates");
@@ -247,11 +253,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const long long nrows = a.nrows;
 
   const int ncolQ = (QTX || UPD) ? p : 0, ncolT = (SK == SK_GAUSS) ? mh : 0;
+  const int mq = (ncolQ + 7) >> 3, ms = (ncolT + 7) >> 3;  // 8-column tiles
   const StageLayout L = stage_layout(K, ncolQ, ncolT, SK == SK_COUNT, T);
   const int NS = a.nstages;
   double* stages = reinterpret_cast<double*>(smem_raw);
-  double* xtile = stages + a.region0_dbl;                         // [2][K][S]
-  double* rfac = xtile + (XT ? 2 * K * S : 0);                    // [3][256]
+  double* xtile = stages + a.region0_dbl;                         // [2][KP][S]
+  double* rfac = xtile + (XT ? 2 * KP * S : 0);                   // [3][256]
   double* rinv = rfac + 3 * 256;                                  // [3][16]
   double* cacc = rinv + 48;                                       // count acc [mh][K]
   uint64_t* bars = reinterpret_cast<uint64_t*>(cacc + ((SK == SK_COUNT) ? mh * K : 0));
@@ -275,6 +282,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int e = tid; e < 256; e += blockDim.x) rfac[512 + e] = a.Rpost[e];
   if (SK == SK_COUNT)
     for (int e = tid; e < mh * K; e += blockDim.x) cacc[e] = 0.0;
+  // zero padding columns (never written by TMA or the phases)
+  for (int s = 0; s < NS; ++s) {
+    double* st = stages + (size_t)s * L.stage;
+    for (int e = tid; e < (KP - K) * S; e += blockDim.x) st[L.offV + K * S + e] = 0.0;
+    for (int e = tid; e < (mq * 8 - ncolQ) * S; e += blockDim.x) st[L.offQ + ncolQ * S + e] = 0.0;
+    for (int e = tid; e < (ms * 8 - ncolT) * S; e += blockDim.x) st[L.offT + ncolT * S + e] = 0.0;
+  }
+  if (XT)
+    for (int b = 0; b < 2; ++b)
+      for (int e = tid; e < (KP - K) * S; e += blockDim.x) xtile[b * KP * S + K * S + e] = 0.0;
   __syncthreads();
   if (tid < 48) {
     const int f = tid / 16, j = tid % 16;
@@ -340,13 +357,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int gtid = gw * 32 + lane;
 
     if (in_trsm_group) {
-      // ---------------------------------------------- A: row solves (warps 0-3)
+      // ---------------------------------------------- A: row solves (warps 0-1)
       for (int it = 0; it < my_tiles; ++it) {
         const int s = it % NS, b = it & 1;
         const long long row0 = (long long)(blockIdx.x + (long long)it * gridDim.x) * T;
         const int valid = (int)(nrows - row0 < T ? nrows - row0 : T);
         const double* stV = stages + (size_t)s * L.stage + L.offV;
-        double* xt = xtile + b * K * S;
+        double* xt = xtile + b * KP * S;
         ptx::mbar_wait(&full[s], (it / NS) & 1);
         if (it >= 2) ptx::named_bar_sync(4 + b, NW * 32);  // X buffer b drained by the U/S/R group
         {
@@ -388,42 +405,48 @@ __global__ void __launch_bounds__(kThreads, 1)
         const double* stQ = st + L.offQ;
         const double* stT = st + L.offT;
         const uint32_t* stC = reinterpret_cast<const uint32_t*>(st + L.offC);
-        double* xt = xtile + b * K * S;
+        double* xt = xtile + b * KP * S;
 
         if (!SPLIT && STORE && gtid < K) ptx::bulk_wait_read0();  // previous tile's store drained
         ptx::mbar_wait(&full[s], (it / NS) & 1);
         if (SPLIT) ptx::named_bar_sync(2 + b, NW * 32);  // solved rows of this tile are in xt
 
-        // ---- U: X = X0 - Q C on tensor cores
+        // ---- U: X = X0 - Q C on tensor cores (rows past the matrix are zero in
+        // the stage and the coefficients past p / K are zero: no masks)
         if (UPD) {
           const double* x0 = SPLIT ? xt : stV;
-          for (int rg = gw; rg < T / 8; rg += GW) {
-            const int r = rg * 8 + g;
-            const bool rv = r < valid;
-            double d[NT][2];
+          auto upd = [&](auto mq_c) {
+            constexpr int MQc = decltype(mq_c)::value;
+            for (int rg = gw; rg < T / 8; rg += GW) {
+              const int r = rg * 8 + g;
+              double av[2 * MQc > 0 ? 2 * MQc : 1];
 #pragma unroll
-            for (int nj = 0; nj < NT; ++nj)
+              for (int ks = 0; ks < 2 * MQc; ++ks) av[ks] = stQ[(ks * 4 + t4) * S + r];
+              double d[NT][2];
 #pragma unroll
-              for (int e = 0; e < 2; ++e) {
-                const int c = nj * 8 + 2 * t4 + e;
-                d[nj][e] = (rv && c < K) ? x0[c * S + r] : 0.0;
-              }
+              for (int nj = 0; nj < NT; ++nj)
 #pragma unroll
-            for (int ks = 0; ks < MQT * 2; ++ks) {
-              if (ks * 4 < p) {
-                const int c = ks * 4 + t4;
-                const double av = (rv && c < p) ? stQ[c * S + r] : 0.0;
+                for (int e = 0; e < 2; ++e) d[nj][e] = x0[(nj * 8 + 2 * t4 + e) * S + r];
 #pragma unroll
-                for (int nj = 0; nj < NT; ++nj) ptx::dmma(d[nj][0], d[nj][1], av, cfr[ks][nj]);
-              }
+              for (int ks = 0; ks < 2 * MQc; ++ks)
+#pragma unroll
+                for (int nj = 0; nj < NT; ++nj) ptx::dmma(d[nj][0], d[nj][1], av[ks], cfr[ks][nj]);
+#pragma unroll
+              for (int nj = 0; nj < NT; ++nj)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) xt[(nj * 8 + 2 * t4 + e) * S + r] = d[nj][e];
             }
-#pragma unroll
-            for (int nj = 0; nj < NT; ++nj)
-#pragma unroll
-              for (int e = 0; e < 2; ++e) {
-                const int c = nj * 8 + 2 * t4 + e;
-                if (c < K) xt[c * S + r] = rv ? d[nj][e] : 0.0;
-              }
+          };
+          switch (mq) {
+            case 0: upd(std::integral_constant<int, 0>{}); break;
+            case 1: upd(std::integral_constant<int, 1>{}); break;
+            case 2: upd(std::integral_constant<int, 2>{}); break;
+            case 3: upd(std::integral_constant<int, 3>{}); break;
+            case 4: upd(std::integral_constant<int, 4>{}); break;
+            case 5: upd(std::integral_constant<int, 5>{}); break;
+            case 6: upd(std::integral_constant<int, 6>{}); break;
+            case 7: upd(std::integral_constant<int, 7>{}); break;
+            default: upd(std::integral_constant<int, 8>{}); break;
           }
           ptx::named_bar_sync(GBAR, GT);
         }
@@ -452,72 +475,73 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::bulk_commit();
         }
 
-        // ---- R: contractions on tensor cores, one 4-row k-step per warp step
+        // ---- R: contractions on tensor cores; each warp owns k-steps
+        // gw, gw + GW, ...; fragments of the next k-step are loaded before the
+        // DMMAs of the current one issue
         if (QTX || GRAM || SK == SK_GAUSS) {
-          // fragments of k-step ks+GW are loaded while the DMMAs of ks issue
-          constexpr int NQ = QTX ? MQT : 1, NS2 = (SK == SK_GAUSS) ? MST : 1;
-          double bx[2][NT], aq[2][NQ], at[2][NS2];
-          auto load = [&](int ks, int slot) {
-            const int r = ks * 4 + t4;
-            const bool rv = r < valid;
+          auto contract = [&](auto m_c) {
+            constexpr int M = decltype(m_c)::value;          // Q or Theta tiles (may be 0)
+            constexpr int MQc = QTX ? M : 0, MSc = (SK == SK_GAUSS) ? M : 0;
+            double bx[2][NT], aq[2][MQc > 0 ? MQc : 1], at[2][MSc > 0 ? MSc : 1];
+            auto load = [&](int ks, int slot) {
+              const int r = ks * 4 + t4;
 #pragma unroll
-            for (int nj = 0; nj < NT; ++nj) {
-              const int c = nj * 8 + g;
-              bx[slot][nj] = (rv && c < K) ? X[c * S + r] : 0.0;
-            }
-            if (QTX) {
+              for (int nj = 0; nj < NT; ++nj) bx[slot][nj] = X[(nj * 8 + g) * S + r];
+              if (QTX) {
 #pragma unroll
-              for (int mi = 0; mi < NQ; ++mi) {
-                const int c = mi * 8 + g;
-                aq[slot][mi] = (mi * 8 < p && rv && c < p) ? stQ[c * S + r] : 0.0;
+                for (int mi = 0; mi < MQc; ++mi) aq[slot][mi] = stQ[(mi * 8 + g) * S + r];
               }
-            }
-            if (SK == SK_GAUSS) {
+              if (SK == SK_GAUSS) {
 #pragma unroll
-              for (int mi = 0; mi < NS2; ++mi) {
-                const int c = mi * 8 + g;
-                at[slot][mi] = (mi * 8 < mh && rv && c < mh) ? stT[c * S + r] : 0.0;
+                for (int mi = 0; mi < MSc; ++mi) at[slot][mi] = stT[(mi * 8 + g) * S + r];
               }
-            }
-          };
-          auto mma = [&](int slot) {
-            if (QTX) {
+            };
+            auto mma = [&](int slot) {
+              if (QTX) {
 #pragma unroll
-              for (int mi = 0; mi < NQ; ++mi)
-                if (mi * 8 < p) {
+                for (int mi = 0; mi < MQc; ++mi)
 #pragma unroll
                   for (int nj = 0; nj < NT; ++nj)
                     ptx::dmma(accq[mi][nj][0], accq[mi][nj][1], aq[slot][mi], bx[slot][nj]);
-                }
-            }
-            if (GRAM) {
+              }
+              if (GRAM) {
 #pragma unroll
-              for (int mi = 0; mi < NT; ++mi)
+                for (int mi = 0; mi < NT; ++mi)
 #pragma unroll
-                for (int nj = 0; nj < NT; ++nj)
-                  if (mi <= nj) ptx::dmma(accg[mi][nj][0], accg[mi][nj][1], bx[slot][mi], bx[slot][nj]);
-            }
-            if (SK == SK_GAUSS) {
+                  for (int nj = 0; nj < NT; ++nj)
+                    if (mi <= nj) ptx::dmma(accg[mi][nj][0], accg[mi][nj][1], bx[slot][mi], bx[slot][nj]);
+              }
+              if (SK == SK_GAUSS) {
 #pragma unroll
-              for (int mi = 0; mi < NS2; ++mi)
-                if (mi * 8 < mh) {
+                for (int mi = 0; mi < MSc; ++mi)
 #pragma unroll
                   for (int nj = 0; nj < NT; ++nj)
                     ptx::dmma(accs[mi][nj][0], accs[mi][nj][1], at[slot][mi], bx[slot][nj]);
-                }
+              }
+            };
+            int ks = gw;
+            if (ks < T / 4) load(ks, 0);
+            while (ks < T / 4) {
+              if (ks + GW < T / 4) load(ks + GW, 1);
+              mma(0);
+              ks += GW;
+              if (ks >= T / 4) break;
+              if (ks + GW < T / 4) load(ks + GW, 0);
+              mma(1);
+              ks += GW;
             }
           };
-          // two-slot ring unrolled by hand so that fragment indices stay static
-          int ks = gw;
-          if (ks < T / 4) load(ks, 0);
-          while (ks < T / 4) {
-            if (ks + GW < T / 4) load(ks + GW, 1);
-            mma(0);
-            ks += GW;
-            if (ks >= T / 4) break;
-            if (ks + GW < T / 4) load(ks + GW, 0);
-            mma(1);
-            ks += GW;
+          const int mcase = QTX ? mq : ((SK == SK_GAUSS) ? ms : 1);
+          switch (mcase) {
+            case 0: contract(std::integral_constant<int, 0>{}); break;
+            case 1: contract(std::integral_constant<int, 1>{}); break;
+            case 2: contract(std::integral_constant<int, 2>{}); break;
+            case 3: contract(std::integral_constant<int, 3>{}); break;
+            case 4: contract(std::integral_constant<int, 4>{}); break;
+            case 5: if (QTX) contract(std::integral_constant<int, QTX ? 5 : 1>{}); break;
+            case 6: if (QTX) contract(std::integral_constant<int, QTX ? 6 : 1>{}); break;
+            case 7: if (QTX) contract(std::integral_constant<int, QTX ? 7 : 1>{}); break;
+            default: if (QTX) contract(std::integral_constant<int, QTX ? 8 : 1>{}); break;
           }
         }
         if (SK == SK_COUNT) {

@@ -91,7 +91,7 @@ __device__ __forceinline__ void prefetch_tmap(const void* tmap) {
 // D(8x8) += A(8x4, row) * B(4x8, col), FP64.  Fragment layout (lane l,
 // g = l>>2, t = l&3):  a = A[g][t],  b = B[t][g],  d = {D[g][2t], D[g][2t+1]}.
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
 }
