@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--kappa", type=float, default=1e2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-gmres", action="store_true", help="skip the C3 GMRES time/restart leg")
+    ap.add_argument("--gmres-restarts", type=int, default=3)
     ap.add_argument("--cpu-rows", type=int, default=1 << 18)
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu")
     return ap.parse_args()
@@ -312,15 +314,30 @@ def main():
         h2d = sum(hv.numel() * 8 for hv in host_v)
         d2h = host_q.numel() * 8 + (args.panels * k) ** 2 * 8
 
+        # Pipelined over three streams: panel i+1 goes H2D while panel i is
+        # orthogonalised, and panel i's finished basis columns go D2H while
+        # later panels run (bcgs2 without overlap never touches earlier
+        # columns, block_orth.cpp:207-226).  PCIe is full duplex.
+        s_in, s_out = torch.cuda.Stream(device=ctx.device), torch.cuda.Stream(device=ctx.device)
+        ev_in = [torch.cuda.Event() for _ in panels]
+        ev_done = [torch.cuda.Event() for _ in panels]
+        slab = store.q_device()
+
         def e2e_step():
             store.reset()
-            for hv, dv in zip(host_v, dev_v):
-                dv[:, : ctx.n_local].copy_(hv, non_blocking=True)
+            with torch.cuda.stream(s_in):
+                for i, (hv, dv) in enumerate(zip(host_v, dev_v)):
+                    dv[:, : ctx.n_local].copy_(hv, non_blocking=True)
+                    ev_in[i].record(s_in)
+            for i, dv in enumerate(dev_v):
+                stream.wait_event(ev_in[i])
                 P.bcgs2(store, dv, intra, theta)
-            slab = store.q_device()
-            host_q.copy_(slab[: args.panels * k, : ctx.n_local], non_blocking=True)
+                ev_done[i].record(stream)
+                with torch.cuda.stream(s_out):
+                    s_out.wait_event(ev_done[i])
+                    host_q[i * k:(i + 1) * k].copy_(slab[i * k:(i + 1) * k, : ctx.n_local], non_blocking=True)
             r = store.r_copy()
-            torch.cuda.current_stream().synchronize()
+            s_out.synchronize()
             return r
 
         e2e_step()
@@ -339,8 +356,58 @@ def main():
             e2e_ms = float(t.item())
         e2e = {"value": algo_bytes / (e2e_ms / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "path": "bo_bcgs2 via ctypes; panels H2D from pinned host, basis Q and R D2H, every step"}
+               "path": "bo_bcgs2 via ctypes; panels H2D from pinned host, basis Q and R D2H, every step; H2D / compute / D2H pipelined per panel on three streams"}
         del host_v, dev_v, host_q
+
+    # ---- C3 (BASELINE configs[2]): s-step GMRES on the 3D 7-point Laplacian
+    # 200^3 (n = 8e6), s = 10, m = 60, bcgs2 + RandCholQR (Gaussian), the
+    # matrix-free stencil for the matrix powers; time per restart cycle.  The
+    # sketch build, MPK, block orthogonalisation, x update and true residual
+    # are all inside the timed region (diagnostics off: they are reported
+    # separately by the reference too).
+    gmres = None
+    side = round(n ** (1.0 / 3.0))
+    if not args.no_gmres and side ** 3 == n and args.s > 0 and 60 % args.s == 0:
+        op = P.Operator.laplace(ctx, 3, side)
+        bvec = ctx.panel(1)
+        bvec[0, : ctx.n_local] = 1.0
+        x0 = ctx.panel(1)
+        kw = dict(m=60, s=args.s, shat=60, scheme="bcgs2_randcholqr", sketch="gaussian", rel_tol=1e-6, seed=0,
+                  diagnostics=False)
+        P.sstep_gmres_solve(op, bvec, x0, max_restarts=1, **kw)  # warm-up (module loading, pools)
+
+        def timed_solve(restarts):
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            g0.record(stream)
+            _, rp = P.sstep_gmres_solve(op, bvec, x0, max_restarts=restarts, **kw)
+            g1.record(stream)
+            torch.cuda.synchronize()
+            ms_ = g0.elapsed_time(g1)
+            if world > 1:
+                t = torch.tensor([ms_], device=ctx.device, dtype=torch.float64)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                ms_ = float(t.item())
+            return ms_, rp
+
+        # per-restart time = (T(1 + R) - T(1)) / R: the solver's one-off setup
+        # (basis slab allocation, first residual) cancels out
+        ms1, _ = timed_solve(1)
+        l0 = ctx.kernel_launches
+        gms, rep = timed_solve(1 + args.gmres_restarts)
+        launches_g = ctx.kernel_launches - l0
+        nr = max(rep["restarts"], 1)
+        gmres = {"workload": f"C3: s-step GMRES, laplace_3d({side}) n={n}, s={args.s}, m=60, bcgs2_randcholqr "
+                             f"(gaussian), matrix-free 7-point MPK, {rep['restarts']} restart cycles",
+                 "ms_per_restart": (gms - ms1) / max(nr - 1, 1), "ms_solve": gms, "ms_solve_1_restart": ms1,
+                 "restarts": rep["restarts"], "iterations": rep["iterations"],
+                 "relres": rep["restart_relres"], "reduce": rep["reduce"],
+                 "phase_ms_per_restart": {kk: v / nr for kk, v in rep["t_ms"].items()},
+                 "gpu_launches": launches_g,
+                 "orth_gb_per_restart": 8.0 * n * algo_words_per_row([10 * j for j in range(60 // args.s)], args.s + 1) / 1e9}
+        del op, bvec, x0
 
     # ---- orthogonality check of the final basis (sanity, untimed)
     q = store.q_device()[: args.panels * k, : ctx.n_local]
@@ -381,6 +448,7 @@ def main():
                                       for kk, d in sorted(kinds.items(), key=lambda kv: -kv[1]["ms"])}},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "gmres": gmres,
             "gpu_launches": launches,
             "allreduces": allreduces,
             "clocks": clocks,

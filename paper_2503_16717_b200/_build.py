@@ -17,12 +17,16 @@ LIB = PKG / "libbo_cuda.so"
 INCLUDE = PKG.parent / "include"
 
 SOURCES = ["bo_capi.cu", "bo_ops.cu", "bo_gmres.cu", "mt64_jump.cpp"]
+# the pass-engine instantiation units: bo_pass_inst.cu compiled once per combination
+INST_UNITS = [f"-DBO_INST_NT={nt} -DBO_INST_T={t}" for nt in (1, 2) for t in (128, 64)] + \
+             [f"-DBO_INST_KC={kc} -DBO_INST_T={t}" for kc in (6, 11, 16) for t in (128, 64)] + ["-DBO_INST_EXACT"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared", "-cudart", "static",
+    "-Xcompiler", "-fPIC",
     "-Xptxas", "-warn-spills",
 ]
+OBJ = PKG.parent / "build" / "obj"
 
 
 def _nvcc() -> str:
@@ -39,18 +43,40 @@ def _stale(target: Path, deps) -> bool:
     return any(Path(d).stat().st_mtime > t for d in deps)
 
 
+def _units():
+    """(object path, source, extra defines) for every compilation unit."""
+    out = [(OBJ / (Path(s).stem + ".o"), CSRC / s, []) for s in SOURCES]
+    for d in INST_UNITS:
+        tag = d.replace("-DBO_INST_", "").replace("=", "").replace(" ", "_").lower()
+        out.append((OBJ / f"bo_pass_inst_{tag}.o", CSRC / "bo_pass_inst.cu", d.split()))
+    return out
+
+
 def build_cuda(force: bool = False, verbose: bool = False) -> Path:
-    deps = [CSRC / s for s in SOURCES if (CSRC / s).exists()]
-    deps += list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + [INCLUDE / "bo_cuda.h"]
-    if not force and not _stale(LIB, deps):
-        return LIB
-    srcs = [str(CSRC / s) for s in SOURCES if (CSRC / s).exists()]
-    tmp = LIB.with_suffix(".so.tmp")
-    cmd = [_nvcc(), *NVCC_FLAGS, "-o", str(tmp), *srcs, "-ldl"]
-    if verbose:
-        print(" ".join(cmd), flush=True)
-    subprocess.run(cmd, check=True, cwd=str(CSRC))
-    tmp.replace(LIB)
+    """Compile every unit for sm_100a (in parallel), then link libbo_cuda.so."""
+    from concurrent.futures import ThreadPoolExecutor
+    headers = list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + [INCLUDE / "bo_cuda.h"]
+    OBJ.mkdir(parents=True, exist_ok=True)
+    nvcc = _nvcc()
+    jobs = []
+    for obj, src, defs in _units():
+        if force or _stale(obj, [src, *headers]):
+            jobs.append([nvcc, *NVCC_FLAGS, *defs, "-c", str(src), "-o", str(obj)])
+
+    def run(cmd):
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True, cwd=str(CSRC))
+
+    if jobs:
+        with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 4))) as ex:
+            list(ex.map(run, jobs))
+    objs = [str(o) for o, _, _ in _units()]
+    if force or jobs or _stale(LIB, objs):
+        tmp = LIB.with_suffix(".so.tmp")
+        run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static", "-o", str(tmp),
+             *objs, "-ldl"])
+        tmp.replace(LIB)
     return LIB
 
 

@@ -22,6 +22,7 @@
 
 #include "bo_internal.h"
 #include "bo_pass.cuh"
+#include "bo_pass_inst.h"
 #include "bo_sketch_gen.cuh"
 #include "mt64_jump.h"
 
@@ -111,7 +112,6 @@ NcclApi& nccl() {
 namespace bo {
 namespace host {
 
-typedef void (*PassFn)(const PassArgs, const CUtensorMap, const CUtensorMap, const CUtensorMap);
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -144,53 +144,27 @@ int make_tmap(CUtensorMap* m, const double* base, uint64_t rows, uint64_t cols, 
   return BO_OK;
 }
 
-template <int NT, int T>
-PassFn pass_fn(int kind) {
-  switch (kind) {
-#define X(nm, a, b, c, d, e, f, g) \
-  case PK_##nm:                    \
-    return pass_kernel<NT, T, a, b, c, d, e, f, g, false>;
-    BO_PASS_KINDS(X)
-#undef X
-  }
-  return nullptr;
-}
-// triangular-solve passes specialised on the panel width (s = 5, 10, 15)
-template <int KC, int T>
-PassFn pass_fn_kc(int kind) {
-  constexpr int NT = KC <= 8 ? 1 : 2;
-  switch (kind) {
-#define X(nm, a, b, c, d, e, f, g)                             \
-  case PK_##nm:                                                \
-    if constexpr (a > 0 || c > 0)                              \
-      return pass_kernel<NT, T, a, b, c, d, e, f, g, false, KC>; \
-    else                                                       \
-      return nullptr;
-    BO_PASS_KINDS(X)
-#undef X
-  }
-  return nullptr;
-}
+// The pass-kernel instantiations live in their own translation units
+// (bo_pass_inst.cu, compiled once per (NT|KC, T) combination in parallel).
 PassFn get_pass_fn(int nt, int T, int kind, bool exact, int K) {
   if (exact)  // standalone apply_inv_upper: bit-exact substitution (dense.cpp:166-186)
-    return nt == 1 ? (PassFn)pass_kernel<1, 64, 1, false, 0, false, false, SK_NONE, true, true>
-                   : (PassFn)pass_kernel<2, 64, 1, false, 0, false, false, SK_NONE, true, true>;
+    return pass_fn_exact(nt);
   const KindInfo& ki = kKindInfo[kind];
   if (ki.npre > 0 || ki.npost > 0) {
     PassFn f = nullptr;
     if (T == 128) {
-      if (K == 6) f = pass_fn_kc<6, 128>(kind);
-      if (K == 11) f = pass_fn_kc<11, 128>(kind);
-      if (K == 16) f = pass_fn_kc<16, 128>(kind);
+      if (K == 6) f = pass_fn_kc6_t128(kind);
+      if (K == 11) f = pass_fn_kc11_t128(kind);
+      if (K == 16) f = pass_fn_kc16_t128(kind);
     } else {
-      if (K == 6) f = pass_fn_kc<6, 64>(kind);
-      if (K == 11) f = pass_fn_kc<11, 64>(kind);
-      if (K == 16) f = pass_fn_kc<16, 64>(kind);
+      if (K == 6) f = pass_fn_kc6_t64(kind);
+      if (K == 11) f = pass_fn_kc11_t64(kind);
+      if (K == 16) f = pass_fn_kc16_t64(kind);
     }
     if (f) return f;
   }
-  if (nt == 1) return T == 128 ? pass_fn<1, 128>(kind) : pass_fn<1, 64>(kind);
-  return T == 128 ? pass_fn<2, 128>(kind) : pass_fn<2, 64>(kind);
+  if (nt == 1) return T == 128 ? pass_fn_nt1_t128(kind) : pass_fn_nt1_t64(kind);
+  return T == 128 ? pass_fn_nt2_t128(kind) : pass_fn_nt2_t64(kind);
 }
 
 // launch one streaming pass (+ its reduction / finalize) on the ctx stream
@@ -562,6 +536,8 @@ extern "C" int bo_ctx_destroy(bo_ctx c) {
   cudaFree(c->tiny);
   cudaFreeHost(c->tiny_host);
   for (int i = 0; i < 3; ++i) cudaFree(c->scratch[i]);
+  cudaFree(c->spare_buf);
+  cudaFree(c->gen_plan.dev);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
   return BO_OK;
@@ -645,47 +621,68 @@ struct Chunk {
 // generate draws [d0, d1) (both even) of the stream seeded with mt_seed
 int gen_stream(bo_ctx ctx, uint64_t mt_seed, const std::vector<std::pair<uint64_t, uint64_t>>& segs,
                GenArgs ga, bo_status* st) {
-  // chunking: ~2 chunks per SM over all segments, each a multiple of 312 draws
+  // chunking: about one chunk per SM over all segments, each a multiple of
+  // 312 draws (mt_stream_kernel: one CTA per chunk)
   uint64_t total = 0;
   for (auto& s : segs) total += s.second - s.first;
   if (total == 0) return BO_OK;
-  const uint64_t target = std::max<uint64_t>(312 * 16, round_up(total / (2 * (uint64_t)ctx->num_sms) + 1, 312));
-  std::vector<Chunk> chunks;
-  for (auto& s : segs)
-    for (uint64_t d = s.first; d < s.second; d += target) chunks.push_back({d, std::min(target, s.second - d)});
-  const int pw = bo::mt64::poly_words();
-  std::vector<uint64_t> polys(chunks.size() * pw), J(chunks.size()), L(chunks.size());
-  // chain x^(J0 + c*target) per segment for cache reuse
-  for (size_t c = 0; c < chunks.size(); ++c) {
-    bo::mt64::jump_poly(chunks[c].J, polys.data() + c * pw);
-    J[c] = chunks[c].J;
-    L[c] = chunks[c].len;
+  const uint64_t target = std::max<uint64_t>(312 * 16, round_up(total / (uint64_t)ctx->num_sms + 1, 312));
+  auto& plan = ctx->gen_plan;
+  if (plan.key_total != total || plan.key_segs != segs || !plan.dev) {
+    // seed-independent part, cached per plan: chunk table + the set-bit
+    // indices of every chunk's jump polynomial x^J mod phi
+    std::vector<Chunk> chunks;
+    for (auto& s : segs)
+      for (uint64_t d = s.first; d < s.second; d += target) chunks.push_back({d, std::min(target, s.second - d)});
+    const size_t nc = chunks.size();
+    const int pw = bo::mt64::poly_words();
+    std::vector<uint64_t> poly(pw), tab(2 * nc + nc + 1);
+    std::vector<uint16_t> idx;
+    idx.reserve(nc * 10240);
+    for (size_t c = 0; c < nc; ++c) {
+      bo::mt64::jump_poly(chunks[c].J, poly.data());
+      tab[c] = chunks[c].J;
+      tab[nc + c] = chunks[c].len;
+      tab[2 * nc + c] = idx.size();
+      for (int w = 0; w < pw; ++w)
+        for (uint64_t b = poly[w]; b; b &= b - 1) idx.push_back((uint16_t)(w * 64 + __builtin_ctzll(b)));
+    }
+    tab[3 * nc] = idx.size();
+    if (plan.dev) cudaFree(plan.dev);
+    plan.dev = nullptr;
+    const size_t words = tab.size() + (idx.size() + 3) / 4 + bo::mt64::prefix_words() + 2;
+    CU(cudaMalloc((void**)&plan.dev, words * 8));
+    CU(cudaMemcpy(plan.dev, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(plan.dev + tab.size(), idx.data(), idx.size() * 2, cudaMemcpyHostToDevice));
+    plan.key_total = total;
+    plan.key_segs = segs;
+    plan.nchunks = nc;
+    plan.pre_off = tab.size() + (idx.size() + 3) / 4;
+    plan.pre_off += plan.pre_off & 1;  // 16-byte alignment for the vector prefix load
   }
-  std::vector<uint64_t> pre(bo::mt64::prefix_words());
-  bo::mt64::prefix(mt_seed, pre.data());
-  uint64_t* dbuf = nullptr;
-  const size_t words = pre.size() + polys.size() + 2 * chunks.size();
-  CU(cudaMallocAsync((void**)&dbuf, words * 8, ctx->stream));
-  CU(cudaMemcpyAsync(dbuf, pre.data(), pre.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
-  CU(cudaMemcpyAsync(dbuf + pre.size(), polys.data(), polys.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
-  CU(cudaMemcpyAsync(dbuf + pre.size() + polys.size(), J.data(), J.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
-  CU(cudaMemcpyAsync(dbuf + pre.size() + polys.size() + J.size(), L.data(), L.size() * 8, cudaMemcpyHostToDevice,
-                     ctx->stream));
-  ga.prefix = dbuf;
-  ga.polys = dbuf + pre.size();
-  ga.chunk_J = dbuf + pre.size() + polys.size();
-  ga.chunk_len = ga.chunk_J + chunks.size();
-  const size_t smem = (size_t)(kPrefixWords + 8 + 2 * kMtN) * 8;
+  const size_t nc = plan.nchunks;
+  uint64_t* dpre = plan.dev + plan.pre_off;
+  // the seed-dependent stream prefix (20248 words of mt19937_64, ~0.1 ms host)
+  plan.prefix.resize(bo::mt64::prefix_words());
+  bo::mt64::prefix(mt_seed, plan.prefix.data());
+  CU(cudaMemcpyAsync(dpre, plan.prefix.data(), plan.prefix.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+  ga.prefix = dpre;
+  ga.polys = nullptr;
+  ga.chunk_J = plan.dev;
+  ga.chunk_len = plan.dev + nc;
+  ga.jidx_off = plan.dev + 2 * nc;
+  ga.jidx = reinterpret_cast<const uint16_t*>(plan.dev + 3 * nc + 1);
+  const size_t smem = (size_t)(kPrefixWords + 8 + kRing * kMtN + 2 * kRing) * 8;
   static bool attr = false;
   if (!attr) {
-    CU(cudaFuncSetAttribute((const void*)sketch_gen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CU(cudaFuncSetAttribute((const void*)mt_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  sketch_gen_kernel<<<(unsigned)chunks.size(), 320, smem, ctx->stream>>>(ga);
+  mt_stream_kernel<<<(unsigned)nc, 1024, smem, ctx->stream>>>(ga);
   CU(cudaGetLastError());
   ctx->launches++;
-  CU(cudaFreeAsync(dbuf, ctx->stream));
-  // keep the host vectors alive until the copies are done
+  // the pageable prefix copy is staged by the driver; one sync keeps the
+  // host vector valid (it is reused by the next build)
   CU(cudaStreamSynchronize(ctx->stream));
   return BO_OK;
 }
@@ -740,12 +737,23 @@ extern "C" int bo_sketch_build(bo_ctx ctx, int kind, uint64_t n, uint64_t shat, 
   std::vector<std::pair<uint64_t, uint64_t>> segs;
   if (kind == BO_SKETCH_GAUSSIAN) {
     s->ldth = ctx->ld;
-    cudaError_t e = cudaMalloc(&s->theta, std::max<uint64_t>(s->ldth * s->mhat, 1) * 8);
-    if (e != cudaSuccess) {
-      delete s;
-      return set_st(st, BO_CUDA, 0, 0.0, "cudaMalloc(theta) failed: %s", cudaGetErrorString(e));
+    const size_t bytes = std::max<uint64_t>(s->ldth * s->mhat, 1) * 8;
+    if (ctx->spare_buf && ctx->spare_bytes >= bytes) {  // recycled from the previous cycle's sketch
+      s->theta = (double*)ctx->spare_buf;
+      s->theta_bytes = ctx->spare_bytes;
+      ctx->spare_buf = nullptr;
+      ctx->spare_bytes = 0;
+    } else {
+      cudaError_t e = cudaMalloc(&s->theta, bytes);
+      if (e != cudaSuccess) {
+        delete s;
+        return set_st(st, BO_CUDA, 0, 0.0, "cudaMalloc(theta) failed: %s", cudaGetErrorString(e));
+      }
+      s->theta_bytes = bytes;
     }
-    cudaMemsetAsync(s->theta, 0, s->ldth * s->mhat * 8, ctx->stream);
+    // every local row is generated; only the padding rows [n_local, ld) need zeros
+    if (s->ldth > nl)
+      cudaMemset2DAsync(s->theta + nl, s->ldth * 8, 0, (s->ldth - nl) * 8, s->mhat, ctx->stream);
     ga.kind = 0;
     ga.mhat = (int)s->mhat;
     ga.scale = 1.0 / std::sqrt(double(s->mhat));
@@ -808,7 +816,8 @@ extern "C" int bo_sketch_from_dense(bo_ctx ctx, const double* theta, uint64_t ld
   s->n = ctx->n_global;
   s->mhat = mhat;
   s->ldth = ctx->ld;
-  CU(cudaMalloc(&s->theta, std::max<uint64_t>(s->ldth * mhat, 1) * 8));
+  s->theta_bytes = std::max<uint64_t>(s->ldth * mhat, 1) * 8;
+  CU(cudaMalloc(&s->theta, s->theta_bytes));
   CU(cudaMemset(s->theta, 0, s->ldth * mhat * 8));
   CU(cudaMemcpy2DAsync(s->theta, s->ldth * 8, theta, ld * 8, ctx->n_local * 8, mhat, cudaMemcpyDeviceToDevice,
                        ctx->stream));
@@ -819,8 +828,20 @@ extern "C" int bo_sketch_from_dense(bo_ctx ctx, const double* theta, uint64_t ld
 
 extern "C" int bo_sketch_destroy(bo_sketch s) {
   if (!s) return BO_OK;
-  cudaStreamSynchronize(s->ctx->stream);
-  if (s->own_theta) cudaFree(s->theta);
+  bo_ctx ctx = s->ctx;
+  cudaStreamSynchronize(ctx->stream);
+  if (s->own_theta && s->theta) {
+    if (!ctx->spare_buf) {  // keep one buffer for the next build
+      ctx->spare_buf = s->theta;
+      ctx->spare_bytes = s->theta_bytes;
+    } else if (ctx->spare_bytes < s->theta_bytes) {
+      cudaFree(ctx->spare_buf);
+      ctx->spare_buf = s->theta;
+      ctx->spare_bytes = s->theta_bytes;
+    } else {
+      cudaFree(s->theta);
+    }
+  }
   cudaFree(s->code);
   cudaFree(s->theta_g);
   delete s;

@@ -10,6 +10,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -82,9 +83,19 @@ __global__ void __launch_bounds__(256) xupdate_kernel(long long n, int q, const 
   __shared__ double ys[256];
   for (int j = threadIdx.x; j < q; j += blockDim.x) ys[j] = y[j];
   __syncthreads();
+  // eight column loads in flight per thread before their FMAs (memory-level
+  // parallelism: one load per thread per iteration leaves HBM idle)
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     double v = x[i];
-    for (int j = 0; j < q; ++j) v = fma(Q[j * ldq + i], ys[j], v);
+    int j = 0;
+    for (; j + 8 <= q; j += 8) {
+      double c[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) c[u] = __ldcs(Q + (j + u) * ldq + i);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v = fma(c[u], ys[j + u], v);
+    }
+    for (; j < q; ++j) v = fma(__ldcs(Q + j * ldq + i), ys[j], v);
     x[i] = v;
   }
 }
@@ -118,11 +129,17 @@ namespace {
 
 constexpr double kHappyTol = 1e-8;  // gmres.cpp:161
 
+bool trace_on() {
+  static const bool on = getenv("BO_TRACE") != nullptr;
+  return on;
+}
+
 struct Gm {
   bo_ctx ctx;
   bo_op op;
   double* part = nullptr;  // per-CTA partial sums (device)
   double* gsum = nullptr;  // allreduce buffer (device)
+  double* ydev = nullptr;  // least-squares solution y (device)
   int grid = 0;
   std::vector<double> hpart;
 };
@@ -429,6 +446,7 @@ extern "C" int bo_sstep_gmres(bo_op op, const double* b, const double* x0, const
   double *r = nullptr, *ax = nullptr, *panel = nullptr, *q1 = nullptr;
   CU(cudaMalloc(&g.part, 4096 * 8));
   CU(cudaMalloc(&g.gsum, 64));
+  CU(cudaMalloc(&g.ydev, (cfg->m + 2) * 8));
   CU(cudaMalloc(&r, ld * 8));
   CU(cudaMalloc(&ax, ld * 8));
   CU(cudaMalloc(&q1, ld * 8));
@@ -440,7 +458,7 @@ extern "C" int bo_sstep_gmres(bo_op op, const double* b, const double* x0, const
     ~Free() {
       for (void* q : p) cudaFree(q);
     }
-  } fr{{g.part, g.gsum, r, ax, q1, panel}};
+  } fr{{g.part, g.gsum, g.ydev, r, ax, q1, panel}};
 
   uint64_t extra[4] = {0, 0, 0, 0};
   // ||A||_F (gmres.cpp:286-288)
@@ -573,17 +591,21 @@ extern "C" int bo_sstep_gmres(bo_op op, const double* b, const double* x0, const
     t0 = std::chrono::steady_clock::now();
     hd::Mat H;
     TRY(assemble_hessenberg(store, q_in, cs.happy ? &cs.happy_col : nullptr, H, st));
+    const double t_h = ms_since(t0);
     std::vector<double> y;
     const double lsq = solve_lsq(H, gamma, y);
-    double* yd = nullptr;
-    CU(cudaMallocAsync((void**)&yd, q_in * 8, ctx->stream));
-    CU(cudaMemcpyAsync(yd, y.data(), q_in * 8, cudaMemcpyHostToDevice, ctx->stream));
-    xupdate_kernel<<<g.grid, 256, 0, ctx->stream>>>((long long)nl, (int)q_in, store->q, (long long)ld, yd, x);
+    const double t_l = ms_since(t0);
+    CU(cudaMemcpyAsync(g.ydev, y.data(), q_in * 8, cudaMemcpyHostToDevice, ctx->stream));
+    xupdate_kernel<<<(unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ctx->num_sms * 8, (nl + 255) / 256)), 256, 0,
+                     ctx->stream>>>((long long)nl, (int)q_in, store->q, (long long)ld, g.ydev, x);
     CU(cudaGetLastError());
     ctx->launches++;
-    CU(cudaFreeAsync(yd, ctx->stream));
+    const double t_k = ms_since(t0);
     CU(cudaStreamSynchronize(ctx->stream));
     rep->t_update += ms_since(t0);
+    if (trace_on())
+      fprintf(stderr, "[bo] cycle %llu update: hessenberg %.3f lsq %.3f launch %.3f sync %.3f ms\n",
+              (unsigned long long)cycle, t_h, t_l - t_h, t_k - t_l, ms_since(t0) - t_k);
     t0 = std::chrono::steady_clock::now();
     TRY(true_residual(g, b, x, ax, r, &gamma, extra, st));
     rep->t_residual += ms_since(t0);

@@ -42,6 +42,20 @@ struct bo_ctx_s {
   std::vector<ProfRec> prof;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
+  // sketch generator plan (seed-independent jump polynomials + chunk table,
+  // device scratch for the per-build prefix and chunk windows)
+  struct GenPlan {
+    uint64_t key_total = 0;
+    std::vector<std::pair<uint64_t, uint64_t>> key_segs;
+    size_t nchunks = 0;
+    size_t pre_off = 0;
+    uint64_t* dev = nullptr;
+    std::vector<uint64_t> prefix;
+  } gen_plan;
+  // one recycled tall sketch buffer (a Gaussian sketch is rebuilt every
+  // restart cycle: cudaMalloc/cudaFree of ~1.4 GB each time would stall)
+  void* spare_buf = nullptr;
+  size_t spare_bytes = 0;
 };
 
 struct bo_sketch_s {
@@ -50,6 +64,7 @@ struct bo_sketch_s {
   uint64_t n = 0, mhat = 0, mc = 0;  // mc: count width (count / count_gauss)
   double* theta = nullptr;            // gaussian local rows (ld x mhat)
   uint64_t ldth = 0;
+  size_t theta_bytes = 0;
   bool own_theta = true;
   uint32_t* code = nullptr;           // count codes (local rows)
   double* theta_g = nullptr;          // count_gauss dense stage (device, mc x mhat)

@@ -38,7 +38,7 @@ struct TileGeom {
 // ---------------------------------------------------------------------------
 // finalize (one CTA): the tiny factorizations after a reduction
 // ---------------------------------------------------------------------------
-__device__ void finalize_dev(const FinArgs& f, double* smem_scratch /* >= 16*16*2 + 256*32 */) {
+static __device__ void finalize_dev(const FinArgs& f, double* smem_scratch /* >= 16*16*2 + 256*32 */) {
   const int tid = threadIdx.x, nth = blockDim.x;
   __shared__ int s_code;
   if (tid == 0) s_code = f.status->code;
@@ -147,7 +147,7 @@ __device__ void finalize_dev(const FinArgs& f, double* smem_scratch /* >= 16*16*
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(256) finalize_kernel(FinArgs f) {
+static __global__ void __launch_bounds__(256) finalize_kernel(FinArgs f) {
   __shared__ double scratch[512 + 4096];
   finalize_dev(f, scratch);
 }
