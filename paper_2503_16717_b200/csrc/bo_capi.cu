@@ -224,16 +224,22 @@ int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st) {
     if (r.exact && tt != 64) continue;
     if (tile_env && tt != tile_env) continue;
     const int S = tt + 4;
+    // row-mode Gram (bo_pass.cuh ROWG): unpadded stages, no X tile
+    const bool rowg = !r.exact && ki.npre > 0 && ki.gram && !ki.qtx && !ki.upd && ki.sk == SK_NONE && !ki.store &&
+                      ki.npost == 0 && (r.K == 6 || r.K == 11) && tt == 128;
     const StageLayout SL = stage_layout(r.K, (ki.qtx || ki.upd) ? r.p : 0, ki.sk == SK_GAUSS ? mh : 0,
-                                        ki.sk == SK_COUNT, tt);
+                                        ki.sk == SK_COUNT, tt, !rowg);
     const size_t stage = (size_t)SL.stage * 8;
-    const bool xt = ki.npre > 0 || ki.upd || ki.npost > 0;
-    const size_t fixed = (xt ? 2 * (size_t)nt * 8 * S * 8 : 0) + (3 * 256 + 48) * 8 +
+    const bool xt = (ki.npre > 0 || ki.upd || ki.npost > 0) && !rowg;
+    // row-major copies of the solve factors (bo_pass.cuh RFT) in K-specialised solve passes
+    const bool rft = !r.exact && (ki.npre > 0 || ki.npost > 0) && (r.K == 6 || r.K == 11 || r.K == 16);
+    const size_t fixed = (xt ? 2 * (size_t)nt * 8 * S * 8 : 0) + (3 * 256 + 48 + (rft ? 3 * 256 : 0)) * 8 +
                          (ki.sk == SK_COUNT ? (size_t)mh * r.K * 8 : 0) + 2 * kMaxStages * 8;
-    const size_t need_red = (size_t)kConsumerWarps * dm_len * 8;
+    const size_t need_red = (size_t)consumer_warps(ki.upd) * dm_len * 8;
     const size_t need_fin = (512 + (size_t)std::max(mh, 1) * 16 + 64) * 8;
     if (avail <= fixed) continue;
     int ns = (int)std::min<size_t>(kMaxStages, (avail - fixed) / stage);
+    if (rowg) ns = ns / consumer_warps(false) * consumer_warps(false);  // one private sub-ring per warp
     if (ns < 1) continue;
     const size_t r0 = round_up(std::max({(size_t)ns * stage, need_red, need_fin}), 128);
     if (r0 + fixed > avail) continue;
@@ -250,6 +256,18 @@ int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st) {
   if (T == 0) return set_st(st, BO_INVALID, 0, 0.0, "pass does not fit in shared memory");
   if (total > avail) return set_st(st, BO_INVALID, 0, 0.0, "pass does not fit in shared memory (%zu bytes)", total);
   a.nstages = NS;
+  {
+    // bytes to keep in flight per SM (L2 prefetch + ring): loaded HBM latency
+    // x per-SM bandwidth with margin (~5 us x 44 GB/s)
+    static const long long pf_kb = [] {
+      const char* e = getenv("BO_PF_KB");
+      return e ? atoll(e) : 0LL;  // off: L2 prefetch measured slower than the ring alone
+    }();
+    const int ncols = r.K + ((ki.qtx || ki.upd) ? r.p : 0) + (ki.sk == SK_GAUSS ? mh : 0);
+    const long long tile_bytes = (long long)T * (8LL * ncols + (ki.sk == SK_COUNT ? 4 : 0));
+    const long long want = (pf_kb * 1024 + tile_bytes - 1) / tile_bytes - NS;
+    a.prefetch_tiles = (int)std::max(0LL, std::min(64LL, want));
+  }
   a.region0_dbl = (int)(region0 / 8);
   a.dm_len = dm_len;
   a.ntiles = (int)((ctx->n_local + T - 1) / T);
@@ -321,7 +339,7 @@ int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st) {
     TRY(make_tmap(&tmT, ki.sk == SK_GAUSS ? r.sk->theta : nullptr, ctx->n_local, mh,
                   ki.sk == SK_GAUSS ? r.sk->ldth : 0, S, st));
   }
-  fn<<<grid, kThreads, total, ctx->stream>>>(a, tmV, tmQ, tmT);
+  fn<<<grid, (consumer_warps(ki.upd) + 1) * 32, total, ctx->stream>>>(a, tmV, tmQ, tmT);
   CU(cudaGetLastError());
   ctx->launches++;
   if (ctx->profiling) {
@@ -484,6 +502,7 @@ extern "C" int bo_ctx_create(int device, int rank, int world, const void* nccl_i
   c->row_end = row_end;
   c->n_local = row_end - row_begin;
   c->ld = round_up(std::max<uint64_t>(c->n_local, 1), 32);
+  if (const char* e = getenv("BO_LD_PAD")) c->ld += round_up((uint64_t)atoll(e), 4);  // layout experiments
   c->num_sms = prop.multiProcessorCount;
   c->smem_optin = prop.sharedMemPerBlockOptin;
   if (stream) {
@@ -492,8 +511,8 @@ extern "C" int bo_ctx_create(int device, int rank, int world, const void* nccl_i
     CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->own_stream = true;
   }
-  CU(cudaMalloc(&c->counter, 64));
-  CU(cudaMemset(c->counter, 0, 64));
+  CU(cudaMalloc(&c->counter, bo::kMaxRedCounters * sizeof(unsigned)));
+  CU(cudaMemset(c->counter, 0, bo::kMaxRedCounters * sizeof(unsigned)));
   CU(cudaMalloc(&c->status, sizeof(DevStatus)));
   CU(cudaMemset(c->status, 0, sizeof(DevStatus)));
   CU(cudaMallocHost(&c->status_host, sizeof(DevStatus)));

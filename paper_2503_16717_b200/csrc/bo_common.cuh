@@ -8,9 +8,13 @@ namespace bo {
 constexpr int kMaxK = 16;        // panel width bound of the streaming passes (s <= 15)
 constexpr int kRld = 16;         // leading dimension of every K x K factor in the workspace
 constexpr int kMaxPTile = 64;    // max projection columns per streaming pass
-constexpr int kConsumerWarps = 8;
-constexpr int kMaxStages = 8;    // shared-memory stage ring depth bound
-constexpr int kThreads = (kConsumerWarps + 1) * 32;  // + 1 producer warp
+// Consumer warps per CTA (+ 1 producer warp).  Update passes use 8 so that
+// the 16 eight-row groups of a 128-row tile split evenly (9 warps cap each
+// thread at 168 registers, which those kernels fit); every other pass uses 7
+// so that 8 warps share the SM and a thread may use up to 255 registers.
+__host__ __device__ constexpr int consumer_warps(bool upd) { return upd ? 8 : 7; }
+constexpr int kMaxConsumerWarps = 8;
+constexpr int kMaxStages = 24;   // shared-memory stage ring depth bound
 
 // Shared-memory stage layout (doubles): every operand block starts on a
 // 128-byte boundary (TMA destination alignment); column stride S = T + 4.
@@ -18,12 +22,13 @@ struct StageLayout {
   int offV, offQ, offT, offC, stage;
 };
 __host__ __device__ inline int ru16(int x) { return (x + 15) & ~15; }
-__host__ __device__ inline StageLayout stage_layout(int K, int ncolQ, int ncolT, bool count, int T) {
+// pad: operand blocks hold a multiple of 8 columns (zero padding for the MMA
+// tiles); row-mode passes (no tensor-core reads) pack the columns tightly.
+__host__ __device__ inline StageLayout stage_layout(int K, int ncolQ, int ncolT, bool count, int T, bool pad = true) {
   const int S = T + 4;
   StageLayout L;
   L.offV = 0;
-  // operand blocks hold a multiple of 8 columns (zero padding for the MMA tiles)
-  L.offQ = ru16(((K + 7) & ~7) * S);
+  L.offQ = ru16((pad ? ((K + 7) & ~7) : K) * S);
   L.offT = L.offQ + ru16(((ncolQ + 7) & ~7) * S);
   L.offC = L.offT + ru16(((ncolT + 7) & ~7) * S);
   L.stage = L.offC + (count ? ru16(T / 2) : 0);
@@ -116,6 +121,7 @@ struct PassArgs {
   unsigned* counter;
   int part_len, off_q, ld_q, off_g, off_s, ld_s;
   int nstages;
+  int prefetch_tiles;      // L2 prefetch lookahead beyond the stage ring (tiles)
   int region0_dbl;         // doubles of shared region 0 (stage ring / reduction / finalize scratch)
   int dm_len;              // tensor-core partial length (excludes the count block)
   int fused_finalize;      // 1: last CTA runs FinArgs

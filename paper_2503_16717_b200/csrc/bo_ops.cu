@@ -16,6 +16,7 @@
 #include "bo_hostdense.h"
 #include "bo_internal.h"
 #include "bo_ptx.cuh"
+#include "bo_reduce.cuh"
 
 
 using namespace bo;
@@ -252,19 +253,7 @@ __global__ void __launch_bounds__(256) wide_contract_kernel(const WideArgs a) {
         if (a.sym && tiles[q][0] < tiles[q][1]) part[j + i * 64] = acc[q][e];
       }
     }
-  __shared__ int s_last;
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) s_last = (atomicAdd(a.counter, 1u) == gridDim.x - 1);
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  for (int e = tid; e < 4096; e += blockDim.x) {
-    double s = 0.0;
-    for (int b = 0; b < (int)gridDim.x; ++b) s += __ldcg(a.partials + (size_t)b * 4096 + e);
-    a.sums[e] = s;
-  }
-  if (tid == 0) *a.counter = 0u;
+  cta_tree_reduce(a.partials, 4096, a.sums, a.counter);
 }
 
 struct WideUpd {

@@ -26,6 +26,7 @@
 
 #include "bo_common.cuh"
 #include "bo_ptx.cuh"
+#include "bo_reduce.cuh"
 #include "bo_tiny.cuh"
 
 namespace bo {
@@ -183,6 +184,32 @@ __device__ __forceinline__ void row_trsm(double (&x)[kMaxK], const double* R, co
 }
 
 
+// Row solve against a row-major copy of R (Rt[j*16 + l] = R[j + l*16] for
+// l > j, Rt[j*16 + j] = 1 / r_jj): the coefficients of step j are contiguous,
+// so they arrive as 16-byte vector loads issued before the step's FMAs
+// (with R read one entry per FMA, every FMA waits on its own shared load).
+template <int KC, int NR>
+__device__ __forceinline__ void row_trsm_t(double (&x)[NR][kMaxK], const double* Rt) {
+#pragma unroll
+  for (int j = 0; j < KC; ++j) {
+    double r[16];
+#pragma unroll
+    for (int l2 = 0; l2 < 16; l2 += 2) {
+      if (l2 + 1 >= j && l2 < KC) {
+        const double2 v = *reinterpret_cast<const double2*>(Rt + j * 16 + l2);
+        r[l2] = v.x;
+        r[l2 + 1] = v.y;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NR; ++q) x[q][j] *= r[j];
+#pragma unroll
+    for (int l = j + 1; l < KC; ++l)
+#pragma unroll
+      for (int q = 0; q < NR; ++q) x[q][l] = fma(-r[l], x[q][j], x[q][l]);
+  }
+}
+
 // several independent rows per thread, interleaved for ILP
 template <bool EXACT, int KC, int NR>
 __device__ __forceinline__ void row_trsm_n(double (&x)[NR][kMaxK], const double* R, const double* rinv, int K) {
@@ -214,24 +241,25 @@ __device__ __forceinline__ void row_trsm_n(double (&x)[NR][kMaxK], const double*
 // ---------------------------------------------------------------------------
 // the pass kernel
 // ---------------------------------------------------------------------------
-// Warp roles (kThreads = 9 warps):
-//   warp 8        producer: one 2-D TMA box per operand per tile (V, Q range,
+// Warp roles (NW = consumer_warps(UPD) consumer warps + 1 producer):
+//   warp NW       producer: one 2-D TMA box per operand per tile (V, Q range,
 //                 Theta) + a 1-D bulk copy of the Count codes, mbarrier ring.
-//   warps 0..7    consumers.  Without a pre-TRSM they form one group that runs
-//                 U -> A' -> S -> R on each tile.  With a pre-TRSM (NPRE > 0)
-//                 warps 0-1 solve rows (A) into a double-buffered X tile while
-//                 warps 2-7 run U/S/R on the previous tile, handed over with
-//                 named-barrier arrive/sync pairs.
+//   warps 0..NW-1 consumers.  Without a pre-TRSM they form one group that
+//                 runs U -> A' -> S -> R on each tile.  With a pre-TRSM
+//                 (NPRE > 0) warps 0-1 solve rows (A) into a double-buffered
+//                 X tile while the others run U/S/R on the previous tile,
+//                 handed over with named-barrier arrive/sync pairs.  Row mode
+//                 (ROWG, below) gives every consumer warp whole tiles.
 // Every staged operand block is zero-padded to a multiple of 8 columns and
 // TMA zero-fills rows past the matrix, so the tensor-core loops need no masks;
 // the number of 8-column tiles is dispatched to a compile-time constant.
 template <int NT, int T, int NPRE, bool UPD, int NPOST, bool QTX, bool GRAM, int SK, bool STORE, bool EXACT,
           int KC = 0>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__((consumer_warps(UPD) + 1) * 32, 1)
     pass_kernel(const __grid_constant__ PassArgs a, const __grid_constant__ CUtensorMap tmV,
                 const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmT) {
   constexpr int S = TileGeom<T>::S;
-  constexpr int NW = kConsumerWarps;
+  constexpr int NW = consumer_warps(UPD);
   constexpr bool SPLIT = NPRE > 0;
   constexpr int GAW = SPLIT ? 2 : 0;       // row-solve warps (2 rows per thread)
   constexpr int GW = NW - GAW;             // warps of the U/S/R group
@@ -241,6 +269,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int KP = NT * 8;               // padded panel width
   constexpr int MQT = kMaxPTile / 8;
   constexpr int MST = 4;
+  // Row mode: a triangular solve followed only by the Gram (P1_GRAM).  The
+  // tensor-core Gram would waste 2/3 of its FLOPs on the 11 -> 16 padding and
+  // leave the solve to two warps; instead every consumer warp takes whole
+  // tiles, solves four rows per thread and accumulates the K(K+1)/2 Gram
+  // entries with FP64 FMAs.
+  constexpr bool ROWG = GRAM && !QTX && !UPD && SK == SK_NONE && !STORE && NPOST == 0 && NPRE > 0 && KC > 0 &&
+                        KC <= 11 && T == 128;
+  constexpr int NG = ROWG ? KC * (KC + 1) / 2 : 1;
   static_assert(!(QTX && UPD), "a pass either projects or updates");
   static_assert(!STORE || XT, "stores come from the X tile");
   static_assert(!SPLIT || T <= GAW * 64, "row-solve group handles two rows per thread");
@@ -254,13 +290,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int ncolQ = (QTX || UPD) ? p : 0, ncolT = (SK == SK_GAUSS) ? mh : 0;
   const int mq = (ncolQ + 7) >> 3, ms = (ncolT + 7) >> 3;  // 8-column tiles
-  const StageLayout L = stage_layout(K, ncolQ, ncolT, SK == SK_COUNT, T);
+  const StageLayout L = stage_layout(K, ncolQ, ncolT, SK == SK_COUNT, T, !ROWG);
   const int NS = a.nstages;
   double* stages = reinterpret_cast<double*>(smem_raw);
   double* xtile = stages + a.region0_dbl;                         // [2][KP][S]
-  double* rfac = xtile + (XT ? 2 * KP * S : 0);                   // [3][256]
+  double* rfac = xtile + ((XT && !ROWG) ? 2 * KP * S : 0);        // [3][256]
   double* rinv = rfac + 3 * 256;                                  // [3][16]
-  double* cacc = rinv + 48;                                       // count acc [mh][K]
+  constexpr bool RFT = KC > 0 && !EXACT && (NPRE > 0 || NPOST > 0);
+  double* rft = rinv + 48;                                        // [3][256] row-major R, 1/r_jj on the diagonal
+  double* cacc = rft + (RFT ? 3 * 256 : 0);                       // count acc [mh][K]
   uint64_t* bars = reinterpret_cast<uint64_t*>(cacc + ((SK == SK_COUNT) ? mh * K : 0));
   uint64_t* full = bars;
   uint64_t* empty = bars + kMaxStages;
@@ -270,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     s_skip = a.status->code != ST_OK;
     for (int s = 0; s < NS; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], NW);
+      ptx::mbar_init(&empty[s], ROWG ? 1 : NW);
     }
     ptx::fence_mbar_init();
   }
@@ -283,19 +321,26 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (SK == SK_COUNT)
     for (int e = tid; e < mh * K; e += blockDim.x) cacc[e] = 0.0;
   // zero padding columns (never written by TMA or the phases)
-  for (int s = 0; s < NS; ++s) {
+  for (int s = 0; s < (ROWG ? 0 : NS); ++s) {
     double* st = stages + (size_t)s * L.stage;
     for (int e = tid; e < (KP - K) * S; e += blockDim.x) st[L.offV + K * S + e] = 0.0;
     for (int e = tid; e < (mq * 8 - ncolQ) * S; e += blockDim.x) st[L.offQ + ncolQ * S + e] = 0.0;
     for (int e = tid; e < (ms * 8 - ncolT) * S; e += blockDim.x) st[L.offT + ncolT * S + e] = 0.0;
   }
-  if (XT)
+  if (XT && !ROWG)
     for (int b = 0; b < 2; ++b)
       for (int e = tid; e < (KP - K) * S; e += blockDim.x) xtile[b * KP * S + K * S + e] = 0.0;
   __syncthreads();
   if (tid < 48) {
     const int f = tid / 16, j = tid % 16;
     rinv[tid] = 1.0 / rfac[f * 256 + j + j * kRld];
+  }
+  if (RFT) {
+    __syncthreads();
+    for (int e = tid; e < 3 * 256; e += blockDim.x) {
+      const int f = e / 256, j = (e % 256) / 16, l = e % 16;  // Rt_f[j*16 + l]
+      rft[e] = l > j ? rfac[f * 256 + j + l * kRld] : (l == j ? rinv[f * 16 + j] : 0.0);
+    }
   }
   __syncthreads();
   if (s_skip) return;  // an earlier pass broke down: this one is a no-op
@@ -304,18 +349,36 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int my_tiles = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
 
   // ------------------------------------------------------------ producer
+  // Warp NW issues the TMA loads.  8 warps per CTA (7 consumers + producer)
+  // put 2 warps on each SM sub-partition, so a thread may use up to 255
+  // registers (a 9th warp would cap every thread at 168 and spill).
+  // Row mode: consumer warp w owns the stages w, w + NW, ... (NS / NW of
+  // them) and its tiles w, w + NW, ... are loaded into them in order (a
+  // private ring per warp: no phase aliasing between warps running apart).
+  const uint32_t box_bytes = (uint32_t)(S * 8 * (K + ncolQ + ncolT));
+  const int nsub = ROWG ? NS / NW : NS;
+  auto stage_of = [&](int it, int& s, int& use) {
+    if (ROWG) {
+      const int w = it % NW, j = it / NW;
+      s = w + NW * (j % nsub);
+      use = j / nsub;
+    } else {
+      s = it % NS;
+      use = it / NS;
+    }
+  };
   if (warp == NW) {
     if (lane == 0) {
       ptx::prefetch_tmap(&tmV);
       if (ncolQ) ptx::prefetch_tmap(&tmQ);
       if (ncolT) ptx::prefetch_tmap(&tmT);
-      const uint32_t box_bytes = (uint32_t)(S * 8 * (K + ncolQ + ncolT));
       for (int it = 0; it < my_tiles; ++it) {
-        const int s = it % NS;
+        int s, use;
+        stage_of(it, s, use);
         const long long row0 = (long long)(blockIdx.x + (long long)it * gridDim.x) * T;
         const long long valid = nrows - row0 < T ? nrows - row0 : T;
         const uint32_t cb = (SK == SK_COUNT) ? (uint32_t)(((valid + 3) & ~3LL) * 4) : 0u;
-        ptx::mbar_wait(&empty[s], ((it / NS) & 1) ^ 1);
+        if (use > 0) ptx::mbar_wait(&empty[s], (use - 1) & 1);
         double* st = stages + (size_t)s * L.stage;
         ptx::mbar_arrive_expect_tx(&full[s], box_bytes + cb);
         ptx::tma_load_2d(st + L.offV, &tmV, (int)row0, 0, &full[s]);
@@ -352,11 +415,59 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int j = 0; j < NT; ++j) accs[i][j][0] = accs[i][j][1] = 0.0;
 
-    const bool in_trsm_group = SPLIT && warp < GAW;
+    const bool in_trsm_group = SPLIT && !ROWG && warp < GAW;
     const int gw = warp - GAW;  // warp index within the U/S/R group
     const int gtid = gw * 32 + lane;
+    double gacc[NG];
+#pragma unroll
+    for (int e = 0; e < NG; ++e) gacc[e] = 0.0;
 
-    if (in_trsm_group) {
+    if constexpr (ROWG) {
+      // ------------------------------------------- row mode (P1_GRAM)
+      // warp w consumes tiles w, w + 8, ...; lane l holds rows l + 32 q
+      // (q < 4): four independent rows per solve step (ILP, and one shared-
+      // memory read of each R entry per four FMAs)
+      constexpr int RQ = KC > 8 ? 1 : 2;  // rows per thread per step (register budget: 168 with 9 warps)
+      for (int j = 0, it = warp; it < my_tiles; ++j, it += NW) {
+        const int s = warp + NW * (j % nsub);
+        const long long row0 = (long long)(blockIdx.x + (long long)it * gridDim.x) * T;
+        const int valid = (int)(nrows - row0 < T ? nrows - row0 : T);
+        const double* stV = stages + (size_t)s * L.stage + L.offV;
+        ptx::mbar_wait(&full[s], (j / nsub) & 1);
+        for (int h = 0; h < T / (32 * RQ); ++h) {
+          // keep the R entries in shared memory (re-read per step) rather than
+          // hoisted into registers next to the K(K+1)/2 accumulators
+          asm volatile("" ::: "memory");
+          double x[RQ][kMaxK];
+#pragma unroll
+          for (int q = 0; q < RQ; ++q)
+#pragma unroll
+            for (int c = 0; c < kMaxK; ++c) x[q][c] = (c < KC) ? stV[c * S + lane + 32 * (h * RQ + q)] : 0.0;
+          row_trsm_t<KC, RQ>(x, rft);
+#pragma unroll
+          for (int q = 0; q < RQ; ++q) {
+            if (lane + 32 * (h * RQ + q) < valid) {
+              int e = 0;
+#pragma unroll
+              for (int i = 0; i < KC; ++i)
+#pragma unroll
+                for (int j = i; j < KC; ++j) {
+                  gacc[e] = fma(x[q][i], x[q][j], gacc[e]);
+                  ++e;
+                }
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&empty[s]);
+      }
+      // warp butterfly (fixed order) of every Gram entry
+#pragma unroll
+      for (int e = 0; e < NG; ++e) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) gacc[e] += __shfl_xor_sync(0xffffffffu, gacc[e], o);
+      }
+    } else if (in_trsm_group) {
       // ---------------------------------------------- A: row solves (warps 0-1)
       for (int it = 0; it < my_tiles; ++it) {
         const int s = it % NS, b = it & 1;
@@ -376,8 +487,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int c = 0; c < kMaxK; ++c) x[q][c] = (c < K && r < T) ? stV[c * S + r] : 0.0;
           }
-          row_trsm_n<EXACT, KC, RPT>(x, rfac, rinv, K);
-          if (NPRE > 1) row_trsm_n<EXACT, KC, RPT>(x, rfac + 256, rinv + 16, K);
+          if constexpr (KC > 0 && !EXACT) {
+            row_trsm_t<KC, RPT>(x, rft);
+            if (NPRE > 1) row_trsm_t<KC, RPT>(x, rft + 256);
+          } else {
+            row_trsm_n<EXACT, KC, RPT>(x, rfac, rinv, K);
+            if (NPRE > 1) row_trsm_n<EXACT, KC, RPT>(x, rfac + 256, rinv + 16, K);
+          }
 #pragma unroll
           for (int q = 0; q < RPT; ++q) {
             const int r = tid + q * GAWX * 32;
@@ -454,13 +570,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ---- A': post-TRSM (thread per row)
         if (NPOST > 0) {
           for (int r = gtid; r < T; r += GT) {
-            double x[kMaxK];
+            double x[1][kMaxK];
 #pragma unroll
-            for (int c = 0; c < kMaxK; ++c) x[c] = (c < K) ? xt[c * S + r] : 0.0;
-            row_trsm<EXACT, KC>(x, rfac + 512, rinv + 32, K);
+            for (int c = 0; c < kMaxK; ++c) x[0][c] = (c < K) ? xt[c * S + r] : 0.0;
+            if constexpr (KC > 0 && !EXACT)
+              row_trsm_t<KC, 1>(x, rft + 512);
+            else
+              row_trsm<EXACT, KC>(x[0], rfac + 512, rinv + 32, K);
 #pragma unroll
             for (int c = 0; c < kMaxK; ++c)
-              if (c < K) xt[c * S + r] = (r < valid) ? x[c] : 0.0;
+              if (c < K) xt[c * S + r] = (r < valid) ? x[0][c] : 0.0;
           }
           ptx::named_bar_sync(GBAR, GT);
         }
@@ -483,7 +602,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             constexpr int M = decltype(m_c)::value;          // Q or Theta tiles (may be 0)
             constexpr int MQc = QTX ? M : 0, MSc = (SK == SK_GAUSS) ? M : 0;
             double bx[2][NT], aq[2][MQc > 0 ? MQc : 1], at[2][MSc > 0 ? MSc : 1];
-            auto load = [&](int ks, int slot) {
+            auto load = [&](int ks, auto slot_c) {
+              constexpr int slot = decltype(slot_c)::value;  // register-resident fragment sets
               const int r = ks * 4 + t4;
 #pragma unroll
               for (int nj = 0; nj < NT; ++nj) bx[slot][nj] = X[(nj * 8 + g) * S + r];
@@ -496,7 +616,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int mi = 0; mi < MSc; ++mi) at[slot][mi] = stT[(mi * 8 + g) * S + r];
               }
             };
-            auto mma = [&](int slot) {
+            auto mma = [&](auto slot_c) {
+              constexpr int slot = decltype(slot_c)::value;
               if (QTX) {
 #pragma unroll
                 for (int mi = 0; mi < MQc; ++mi)
@@ -520,14 +641,14 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             };
             int ks = gw;
-            if (ks < T / 4) load(ks, 0);
+            if (ks < T / 4) load(ks, std::integral_constant<int, 0>{});
             while (ks < T / 4) {
-              if (ks + GW < T / 4) load(ks + GW, 1);
-              mma(0);
+              if (ks + GW < T / 4) load(ks + GW, std::integral_constant<int, 1>{});
+              mma(std::integral_constant<int, 0>{});
               ks += GW;
               if (ks >= T / 4) break;
-              if (ks + GW < T / 4) load(ks + GW, 0);
-              mma(1);
+              if (ks + GW < T / 4) load(ks + GW, std::integral_constant<int, 0>{});
+              mma(std::integral_constant<int, 1>{});
               ks += GW;
             }
           };
@@ -595,7 +716,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (i < a.ld_q && j < 16) red[warp * dm_len + a.off_q + i + j * a.ld_q] = accq[mi][nj][e];
           }
     }
-    if (GRAM) {
+    if (ROWG) {
+      if (lane == 0) {
+        int e = 0;
+#pragma unroll
+        for (int i = 0; i < KC; ++i)
+#pragma unroll
+          for (int j = i; j < KC; ++j) {
+            red[warp * dm_len + a.off_g + i + j * 16] = gacc[e];
+            red[warp * dm_len + a.off_g + j + i * 16] = gacc[e];
+            ++e;
+          }
+      }
+    } else if (GRAM) {
 #pragma unroll
       for (int mi = 0; mi < NT; ++mi)
 #pragma unroll
@@ -635,22 +768,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 
-  // ---- cross-CTA reduction by the last CTA (fixed CTA order: deterministic)
-  __shared__ int s_last;
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) s_last = (atomicAdd(a.counter, 1u) == gridDim.x - 1);
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  for (int e = tid; e < a.part_len; e += blockDim.x) {
-    double sum = 0.0;
-    for (int b = 0; b < (int)gridDim.x; ++b) sum += __ldcg(a.partials + (size_t)b * a.part_len + e);
-    a.sums[e] = sum;
-  }
-  if (tid == 0) *a.counter = 0u;
-  __threadfence();
-  __syncthreads();
+  // ---- cross-CTA reduction (fixed two-level tree: deterministic)
+  if (!cta_tree_reduce(a.partials, a.part_len, a.sums, a.counter)) return;
   if (a.fused_finalize) finalize_dev(a.fin, reinterpret_cast<double*>(smem_raw));
 }
 

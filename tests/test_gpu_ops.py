@@ -222,9 +222,13 @@ def _gmres(gpu, mk, orc, k2d, **kw):
     return ctx, x, rep, want
 
 
-def _envelope(i):
+def _envelope(i, scheme=None):
     """relres tolerance per restart: 10x the reference's own reorder / libm
-    envelope (<=2.6e-11 to restart 5, 2.6e-10, 1.1e-8, then 1.6e-4)"""
+    envelope (<=2.6e-11 to restart 5, 2.6e-10, 1.1e-8, then 1.6e-4).
+    Two-stage RandBCGS is more sensitive: its own FMA/non-FMA libm envelope
+    is 6.1e-9, 3.6e-7, 7.7e-4, 1.3e-3 at restarts 6-9 (scripts/isa_envelope.py)."""
+    if scheme == "twostage_randbcgs":
+        return ([1e-10] * 6 + [6.1e-8, 3.6e-6, 7.7e-3, 1.3e-2] + [1.3e-2] * 100)[i]
     return ([1e-10] * 6 + [1e-8, 1e-6, 2e-3, 2e-3] + [2e-3] * 100)[i]
 
 
@@ -268,7 +272,7 @@ def test_gmres_two_stage_c1(gpu, mk, orc, scheme):
     assert rep["iterations"] == want.iterations
     assert rep["reduce"] == want.reduce
     for i, (g, w) in enumerate(zip(rep["restart_relres"], want.relres)):
-        assert abs(g - w) <= _envelope(i) * abs(w), (i, g, w)
+        assert abs(g - w) <= _envelope(i, scheme) * abs(w), (i, g, w)
 
 
 def test_gmres_randcholqr_s10_converges(gpu, mk, orc):
