@@ -52,16 +52,20 @@ def _units():
     return out
 
 
-def build_cuda(force: bool = False, verbose: bool = False) -> Path:
-    """Compile every unit for sm_100a (in parallel), then link libbo_cuda.so."""
+def build_cuda(force: bool = False, verbose: bool = False, defines=(), tag: str = "") -> Path:
+    """Compile every unit for sm_100a (in parallel), then link libbo_cuda.so.
+    defines/tag: experiment variants (build/obj_<tag>, libbo_cuda_<tag>.so)."""
+    obj_dir = OBJ if not tag else OBJ.parent / f"obj_{tag}"
+    lib = LIB if not tag else PKG / f"libbo_cuda_{tag}.so"
     from concurrent.futures import ThreadPoolExecutor
     headers = list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + [INCLUDE / "bo_cuda.h"]
-    OBJ.mkdir(parents=True, exist_ok=True)
+    obj_dir.mkdir(parents=True, exist_ok=True)
     nvcc = _nvcc()
     jobs = []
-    for obj, src, defs in _units():
+    units = [(obj_dir / o.name, src, defs) for o, src, defs in _units()]
+    for obj, src, defs in units:
         if force or _stale(obj, [src, *headers]):
-            jobs.append([nvcc, *NVCC_FLAGS, *defs, "-c", str(src), "-o", str(obj)])
+            jobs.append([nvcc, *NVCC_FLAGS, *defines, *defs, "-c", str(src), "-o", str(obj)])
 
     def run(cmd):
         if verbose:
@@ -71,13 +75,13 @@ def build_cuda(force: bool = False, verbose: bool = False) -> Path:
     if jobs:
         with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 4))) as ex:
             list(ex.map(run, jobs))
-    objs = [str(o) for o, _, _ in _units()]
-    if force or jobs or _stale(LIB, objs):
-        tmp = LIB.with_suffix(".so.tmp")
+    objs = [str(o) for o, _, _ in units]
+    if force or jobs or _stale(lib, objs):
+        tmp = lib.with_suffix(".so.tmp")
         run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static", "-o", str(tmp),
              *objs, "-ldl"])
-        tmp.replace(LIB)
-    return LIB
+        tmp.replace(lib)
+    return lib
 
 
 def build_examples() -> None:

@@ -126,7 +126,7 @@ def load(path: str | os.PathLike | None = None) -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    p = Path(path) if path else Path(os.environ.get("BO_LIB", LIB_PATH))  # BO_LIB: experiment builds
     if not p.exists():
         raise RuntimeError(
             f"CUDA extension {p} is missing: run `python -m paper_2503_16717_b200._build` "

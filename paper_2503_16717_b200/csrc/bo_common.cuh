@@ -12,8 +12,14 @@ constexpr int kMaxPTile = 64;    // max projection columns per streaming pass
 // the 16 eight-row groups of a 128-row tile split evenly (9 warps cap each
 // thread at 168 registers, which those kernels fit); every other pass uses 7
 // so that 8 warps share the SM and a thread may use up to 255 registers.
-__host__ __device__ constexpr int consumer_warps(bool upd) { return upd ? 8 : 7; }
-constexpr int kMaxConsumerWarps = 8;
+#ifndef BO_NW_UPD
+#define BO_NW_UPD 8
+#endif
+#ifndef BO_NW_OTHER
+#define BO_NW_OTHER 7
+#endif
+__host__ __device__ constexpr int consumer_warps(bool upd) { return upd ? BO_NW_UPD : BO_NW_OTHER; }
+constexpr int kMaxConsumerWarps = BO_NW_UPD > BO_NW_OTHER ? BO_NW_UPD : BO_NW_OTHER;
 constexpr int kMaxStages = 24;   // shared-memory stage ring depth bound
 
 // Shared-memory stage layout (doubles): every operand block starts on a

@@ -27,6 +27,10 @@
 #include "bo_common.cuh"
 #include "bo_ptx.cuh"
 #include "bo_reduce.cuh"
+
+#ifndef BO_GAW
+#define BO_GAW 2
+#endif
 #include "bo_tiny.cuh"
 
 namespace bo {
@@ -261,7 +265,7 @@ __global__ void __launch_bounds__((consumer_warps(UPD) + 1) * 32, 1)
   constexpr int S = TileGeom<T>::S;
   constexpr int NW = consumer_warps(UPD);
   constexpr bool SPLIT = NPRE > 0;
-  constexpr int GAW = SPLIT ? 2 : 0;       // row-solve warps (2 rows per thread)
+  constexpr int GAW = SPLIT ? BO_GAW : 0;  // row-solve warps (one per SM sub-partition: one row per thread)
   constexpr int GW = NW - GAW;             // warps of the U/S/R group
   constexpr int GT = GW * 32;
   constexpr int GBAR = SPLIT ? 6 : 1;      // named barrier of the U/S/R group
