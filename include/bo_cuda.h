@@ -212,6 +212,13 @@ int bo_op_csr(bo_ctx ctx, uint64_t ncols, const int64_t* row_ptr, const int64_t*
 /* matrix-free 2D 5-point / 3D 7-point Laplacian on a k^dims grid
  * (problems.cpp:65-113), bit-identical to spmv on the CSR of laplace_2d/3d */
 int bo_op_laplace(bo_ctx ctx, int dims, uint64_t k, bo_op* out, bo_status* st);
+/* matrix-free constant-coefficient 5-point (2D) / 7-point (3D) stencil on a
+ * k^dims grid; coeffs (2*dims+1) in ascending column order, 3D: (i-1, j-1,
+ * l-1, self, l+1, j+1, i+1).  Bit-identical to spmv on the CSR that
+ * CsrMatrix::from_triplets (sparse.cpp:13-42) builds from the same entries.
+ * Config 5's nonsymmetric convection-diffusion operator (absent from the
+ * reference, SURVEY finding 4) is coeffs = (-1-w, -1-w, -1-w, 6, -1+w, -1+w, -1+w). */
+int bo_op_stencil(bo_ctx ctx, int dims, uint64_t k, const double* coeffs, bo_op* out, bo_status* st);
 int bo_op_destroy(bo_op op);
 /* spmv (sparse.cpp:51-63): y = A x (local rows; x is the local shard, halo
  * exchanged internally when world > 1) */

@@ -407,6 +407,55 @@ class Oracle:
         self._fn("csr_free", None, [vp])(h)
         return rp.astype(np.int64), ci.astype(np.int64), vv
 
+    @staticmethod
+    def stencil_csr(k, dims, coeffs):
+        """CSR (row_ptr, col, val) of a constant-coefficient 5/7-point stencil on
+        a k^dims grid, entries in ascending column order per row (what
+        CsrMatrix::from_triplets, sparse.cpp:13-42, makes of the row-major
+        triplet list; problems.cpp:65-113 for the Laplacian coefficients).
+        Config 5's convection-diffusion operator is not in the reference
+        (SURVEY finding 4): this generator is test infrastructure."""
+        c = np.asarray(coeffs, dtype=np.float64)
+        n = k ** dims
+        me = np.arange(n, dtype=np.int64)
+        if dims == 3:
+            i, j, l = me // (k * k), (me // k) % k, me % k
+            nb = [(i > 0, -k * k), (j > 0, -k), (l > 0, -1), (np.ones(n, bool), 0), (l + 1 < k, 1),
+                  (j + 1 < k, k), (i + 1 < k, k * k)]
+        else:
+            i, j = me // k, me % k
+            nb = [(i > 0, -k), (j > 0, -1), (np.ones(n, bool), 0), (j + 1 < k, 1), (i + 1 < k, k)]
+        present = np.stack([m for m, _ in nb], axis=1)
+        cols = me[:, None] + np.array([o for _, o in nb])[None, :]
+        vals = np.broadcast_to(c[None, :], present.shape)
+        counts = present.sum(axis=1)
+        rp = np.zeros(n + 1, dtype=np.int64)
+        np.cumsum(counts, out=rp[1:])
+        return rp, cols[present].astype(np.int64), vals[present].astype(np.float64)
+
+    def csr_from_triplets(self, rp, ci, vv, ncols=None):
+        """round-trip through the oracle's from_triplets (sorted, duplicates summed)"""
+        ncols = ncols or (len(rp) - 1)
+        h, keep = self._csr_handle(rp, ci, vv, ncols)
+        if self.which == "orc":
+            a = h.contents
+            n, nnz = a.nrows, a.nnz
+            out = (np.ctypeslib.as_array(a.row_ptr, shape=(n + 1,)).astype(np.int64),
+                   np.ctypeslib.as_array(a.col_idx, shape=(nnz,)).astype(np.int64),
+                   np.ctypeslib.as_array(a.values, shape=(nnz,)).copy())
+        else:
+            nr, nc = sz(), sz()
+            nnz = self._fn("csr_info", sz, [vp, szp, szp])(h, C.byref(nr), C.byref(nc))
+            r = np.zeros(nr.value + 1, dtype=np.uint64)
+            c = np.zeros(nnz, dtype=np.uint64)
+            v = np.zeros(nnz)
+            self._fn("csr_arrays", None, [vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), dp])(
+                h, r.ctypes.data_as(C.POINTER(C.c_uint64)), c.ctypes.data_as(C.POINTER(C.c_uint64)),
+                v.ctypes.data_as(dp))
+            out = (r.astype(np.int64), c.astype(np.int64), v)
+        self._csr_free(h)
+        return out
+
     def _csr_handle(self, rp, ci, vv, ncols):
         n = len(rp) - 1
         rows = np.repeat(np.arange(n, dtype=np.uint64), np.diff(rp)).astype(np.uint64)

@@ -111,6 +111,7 @@ _SIGS = {
     "bo_two_stage_finish": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, dp, SP]),
     "bo_op_csr": (C.c_int, [vp, u64, C.POINTER(i64), C.POINTER(i64), dp, C.POINTER(vp), SP]),
     "bo_op_laplace": (C.c_int, [vp, C.c_int, u64, C.POINTER(vp), SP]),
+    "bo_op_stencil": (C.c_int, [vp, C.c_int, u64, dp, C.POINTER(vp), SP]),
     "bo_op_destroy": (C.c_int, [vp]),
     "bo_spmv": (C.c_int, [vp, vp, vp, SP]),
     "bo_mpk": (C.c_int, [vp, vp, u64, vp, u64, SP]),

@@ -576,6 +576,13 @@ def two_stage_cycle(store: BasisStore, panels, preproc, theta=None, reorthogonal
 
 
 # -------------------------------------------------------------- operator --
+def convdiff_coeffs(w: float = 0.3):
+    """7-point coefficients (i-1, j-1, l-1, self, l+1, j+1, i+1) of the config-5
+    convection-diffusion operator: -Laplace(u) + b . grad(u), constant wind b
+    along (1, 1, 1), central differences, cell Peclet w = b h / 2."""
+    lo, hi = -1.0 - w, -1.0 + w
+    return np.array([lo, lo, lo, 6.0, hi, hi, hi])
+
 class Operator:
     """CsrMatrix rows of this shard (or the matrix-free Laplacian) on device."""
 
@@ -598,6 +605,22 @@ class Operator:
         h = C.c_void_p()
         _call(ctx.lib.bo_op_laplace, ctx.h, dims, k, C.byref(h))
         return cls(ctx, h)
+
+    @classmethod
+    def stencil(cls, ctx: Context, dims: int, k: int, coeffs):
+        """constant-coefficient 5/7-point stencil, coeffs in ascending column order"""
+        c = np.ascontiguousarray(coeffs, dtype=np.float64)
+        if c.shape != (2 * dims + 1,):
+            raise ValueError(f"need {2 * dims + 1} stencil coefficients")
+        h = C.c_void_p()
+        _call(ctx.lib.bo_op_stencil, ctx.h, dims, k, _dp(c), C.byref(h))
+        return cls(ctx, h)
+
+    @classmethod
+    def convdiff(cls, ctx: Context, k: int, w: float = 0.3):
+        """config 5: nonsymmetric 3D convection-diffusion, central differences
+        (diagonal 6, lower neighbours -1-w, upper neighbours -1+w)"""
+        return cls.stencil(ctx, 3, k, convdiff_coeffs(w))
 
     def spmv(self, x, y=None):
         y = self.ctx.panel(1) if y is None else y

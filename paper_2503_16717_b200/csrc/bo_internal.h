@@ -86,7 +86,8 @@ struct bo_basis_s {
 
 struct bo_op_s {
   bo_ctx ctx = nullptr;
-  int kind = 0;  // 0 csr, 1 laplace
+  int kind = 0;  // 0 csr, 1 constant-coefficient stencil (Laplacian, convection-diffusion)
+  double coef[7] = {0, 0, 0, 0, 0, 0, 0};  // stencil coefficients, ascending column order
   int dims = 0;
   uint64_t k = 0;
   uint64_t ncols = 0;

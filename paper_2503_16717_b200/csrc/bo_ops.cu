@@ -54,17 +54,24 @@ __global__ void __launch_bounds__(256) spmv_csr_kernel(long long nrows, const in
   }
 }
 
-// Matrix-free 2D 5-point / 3D 7-point Laplacian (problems.cpp:65-113): same
-// entries, same ascending-column order, so bit-identical to the CSR SpMV.
+// Matrix-free constant-coefficient stencils on a k^dims grid: the 2D 5-point /
+// 3D 7-point Laplacian (problems.cpp:65-113) and the 3D convection-diffusion
+// operator of config 5.  Coefficients c[] are in ascending column order,
+// 3D: (i-1, j-1, l-1, self, l+1, j+1, i+1), 2D: (i-1, j-1, self, j+1, i+1);
+// the row sum is formed in that order from +0.0 with unfused mul/add, so the
+// result is bit-identical to spmv (sparse.cpp:57-61) on the same CSR.
 // xext holds [halo_lo rows | local rows | halo_hi rows].  The grid
 // coordinates of a row come from divisions by k and k^2; IDX = uint32_t when
 // the global row count fits (the 64-bit division subroutine would otherwise
 // dominate a kernel that moves only 16 bytes per row).
+struct Stencil {
+  double c[7];
+};
+
 template <typename IDX>
-__global__ void __launch_bounds__(256) spmv_laplace_kernel(int dims, IDX k, IDX row_begin, IDX nrows, IDX halo_lo,
-                                                           const double* __restrict__ xext,
+__global__ void __launch_bounds__(256) spmv_stencil_kernel(int dims, IDX k, IDX row_begin, IDX nrows, IDX halo_lo,
+                                                           const Stencil st, const double* __restrict__ xext,
                                                            double* __restrict__ y) {
-  const double diag = dims == 2 ? 4.0 : 6.0;
   const IDX off = row_begin - halo_lo;  // xext index = global - off
   const IDX stride = (IDX)gridDim.x * blockDim.x;
   for (IDX r = (IDX)blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += stride) {
@@ -74,20 +81,20 @@ __global__ void __launch_bounds__(256) spmv_laplace_kernel(int dims, IDX k, IDX 
     if (dims == 3) {
       const IDX kk = k * k;
       const IDX i = me / kk, rem = me - i * kk, j = rem / k, l = rem - j * k;
-      if (i > 0) s = __dadd_rn(s, __dmul_rn(-1.0, __ldg(xm - kk)));
-      if (j > 0) s = __dadd_rn(s, __dmul_rn(-1.0, __ldg(xm - k)));
-      if (l > 0) s = __dadd_rn(s, __dmul_rn(-1.0, __ldg(xm - 1)));
-      s = __dadd_rn(s, __dmul_rn(diag, __ldg(xm)));
-      if (l + 1 < k) s = __dadd_rn(s, __dmul_rn(-1.0, __ldg(xm + 1)));
-      if (j + 1 < k) s = __dadd_rn(s, __dmul_rn(-1.0, __ldg(xm + k)));
-      if (i + 1 < k) s = __dadd_rn(s, __dmul_rn(-1.0, __ldg(xm + kk)));
+      if (i > 0) s = __dadd_rn(s, __dmul_rn(st.c[0], __ldg(xm - kk)));
+      if (j > 0) s = __dadd_rn(s, __dmul_rn(st.c[1], __ldg(xm - k)));
+      if (l > 0) s = __dadd_rn(s, __dmul_rn(st.c[2], __ldg(xm - 1)));
+      s = __dadd_rn(s, __dmul_rn(st.c[3], __ldg(xm)));
+      if (l + 1 < k) s = __dadd_rn(s, __dmul_rn(st.c[4], __ldg(xm + 1)));
+      if (j + 1 < k) s = __dadd_rn(s, __dmul_rn(st.c[5], __ldg(xm + k)));
+      if (i + 1 < k) s = __dadd_rn(s, __dmul_rn(st.c[6], __ldg(xm + kk)));
     } else {
       const IDX i = me / k, j = me - i * k;
-      if (i > 0) s = __dadd_rn(s, __dmul_rn(-1.0, __ldg(xm - k)));
-      if (j > 0) s = __dadd_rn(s, __dmul_rn(-1.0, __ldg(xm - 1)));
-      s = __dadd_rn(s, __dmul_rn(diag, __ldg(xm)));
-      if (j + 1 < k) s = __dadd_rn(s, __dmul_rn(-1.0, __ldg(xm + 1)));
-      if (i + 1 < k) s = __dadd_rn(s, __dmul_rn(-1.0, __ldg(xm + k)));
+      if (i > 0) s = __dadd_rn(s, __dmul_rn(st.c[0], __ldg(xm - k)));
+      if (j > 0) s = __dadd_rn(s, __dmul_rn(st.c[1], __ldg(xm - 1)));
+      s = __dadd_rn(s, __dmul_rn(st.c[2], __ldg(xm)));
+      if (j + 1 < k) s = __dadd_rn(s, __dmul_rn(st.c[3], __ldg(xm + 1)));
+      if (i + 1 < k) s = __dadd_rn(s, __dmul_rn(st.c[4], __ldg(xm + k)));
     }
     y[r] = s;
   }
@@ -97,20 +104,25 @@ __global__ void __launch_bounds__(256) spmv_laplace_kernel(int dims, IDX k, IDX 
 // shard starts on a multiple of 4): the centre, +-k and +-k^2 neighbours come
 // in as 16-byte vector loads, so each thread keeps ~12 loads in flight instead
 // of 7 dependent-address ones per row.  Every row's sum is still formed in the
-// reference order with unfused mul/add (bit-identical to spmv_laplace_kernel).
-__global__ void __launch_bounds__(256) spmv_laplace4_kernel(int dims, uint32_t k, uint32_t row_begin, uint32_t ngroups,
-                                                            uint32_t halo_lo, const double* __restrict__ xext,
+// reference order with unfused mul/add (bit-identical to spmv_stencil_kernel).
+__global__ void __launch_bounds__(256) spmv_stencil4_kernel(int dims, uint32_t k, uint32_t row_begin, uint32_t ngroups,
+                                                            uint32_t halo_lo, const Stencil st,
+                                                            const double* __restrict__ xext,
                                                             double* __restrict__ y) {
-  const double diag = dims == 2 ? 4.0 : 6.0;
+  // 3D order (i-1, j-1, l-1, self, l+1, j+1, i+1); 2D uses the j / l slots
+  const double ci_lo = dims == 3 ? st.c[0] : 0.0, cj_lo = dims == 3 ? st.c[1] : st.c[0];
+  const double cl_lo = dims == 3 ? st.c[2] : st.c[1], cself = dims == 3 ? st.c[3] : st.c[2];
+  const double cl_hi = dims == 3 ? st.c[4] : st.c[3], cj_hi = dims == 3 ? st.c[5] : st.c[4];
+  const double ci_hi = dims == 3 ? st.c[6] : 0.0;
   const uint32_t kk = k * k;
   const uint32_t stride = gridDim.x * blockDim.x;
   for (uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x; gi < ngroups; gi += stride) {
     const uint32_t r = 4 * gi, me = row_begin + r;
     const double* xm = xext + (r + halo_lo);  // x[me]
-    uint32_t i, j, l0;
+    uint32_t j, l0;
     bool has_i_lo, has_i_hi;
     if (dims == 3) {
-      i = me / kk;
+      const uint32_t i = me / kk;
       const uint32_t rem = me - i * kk;
       j = rem / k;
       l0 = rem - j * k;
@@ -119,7 +131,6 @@ __global__ void __launch_bounds__(256) spmv_laplace4_kernel(int dims, uint32_t k
     } else {
       j = me / k;  // the 2-D line index plays the role of j (neighbours +-k)
       l0 = me - j * k;
-      i = 0;
       has_i_lo = has_i_hi = false;
     }
     const bool has_j_lo = j > 0, has_j_hi = j + 1 < k;
@@ -152,13 +163,13 @@ __global__ void __launch_bounds__(256) spmv_laplace4_kernel(int dims, uint32_t k
     for (int t = 0; t < 4; ++t) {
       const uint32_t l = l0 + t;
       double s = 0.0;
-      if (has_i_lo) s = __dadd_rn(s, __dmul_rn(-1.0, il[t]));
-      if (has_j_lo) s = __dadd_rn(s, __dmul_rn(-1.0, jl[t]));
-      if (l > 0) s = __dadd_rn(s, __dmul_rn(-1.0, c[t]));
-      s = __dadd_rn(s, __dmul_rn(diag, c[t + 1]));
-      if (l + 1 < k) s = __dadd_rn(s, __dmul_rn(-1.0, c[t + 2]));
-      if (has_j_hi) s = __dadd_rn(s, __dmul_rn(-1.0, jh[t]));
-      if (has_i_hi) s = __dadd_rn(s, __dmul_rn(-1.0, ih[t]));
+      if (has_i_lo) s = __dadd_rn(s, __dmul_rn(ci_lo, il[t]));
+      if (has_j_lo) s = __dadd_rn(s, __dmul_rn(cj_lo, jl[t]));
+      if (l > 0) s = __dadd_rn(s, __dmul_rn(cl_lo, c[t]));
+      s = __dadd_rn(s, __dmul_rn(cself, c[t + 1]));
+      if (l + 1 < k) s = __dadd_rn(s, __dmul_rn(cl_hi, c[t + 2]));
+      if (has_j_hi) s = __dadd_rn(s, __dmul_rn(cj_hi, jh[t]));
+      if (has_i_hi) s = __dadd_rn(s, __dmul_rn(ci_hi, ih[t]));
       out[t] = s;
     }
     *reinterpret_cast<double2*>(y + r) = make_double2(out[0], out[1]);
@@ -626,7 +637,7 @@ extern "C" int bo_op_csr(bo_ctx ctx, uint64_t ncols, const int64_t* row_ptr, con
   return BO_OK;
 }
 
-extern "C" int bo_op_laplace(bo_ctx ctx, int dims, uint64_t k, bo_op* out, bo_status* st) {
+extern "C" int bo_op_stencil(bo_ctx ctx, int dims, uint64_t k, const double* coeffs, bo_op* out, bo_status* st) {
   ok_st(st);
   *out = nullptr;
   CU(cudaSetDevice(ctx->device));
@@ -639,6 +650,7 @@ extern "C" int bo_op_laplace(bo_ctx ctx, int dims, uint64_t k, bo_op* out, bo_st
   op->dims = dims;
   op->k = k;
   op->ncols = n;
+  for (int q = 0; q < 2 * dims + 1; ++q) op->coef[q] = coeffs[q];
   const uint64_t plane = dims == 2 ? k : k * k;
   const long long need_lo = std::max<long long>(0, (long long)ctx->row_begin - (long long)plane);
   const long long need_hi = std::min<long long>((long long)n, (long long)ctx->row_end + (long long)plane);
@@ -648,23 +660,33 @@ extern "C" int bo_op_laplace(bo_ctx ctx, int dims, uint64_t k, bo_op* out, bo_st
     bo_op_destroy(op);
     return rc;
   }
-  // ||A||_F^2 of this shard's rows (all entries are small integers: exact in any order)
+  // ||A||_F^2 of this shard's rows: entries squared and summed in row order,
+  // column-ascending within a row (the CSR value order, gmres.cpp:286-288)
   double fro = 0.0;
-  const double diag = dims == 2 ? 4.0 : 6.0;
   for (uint64_t me = ctx->row_begin; me < ctx->row_end; ++me) {
-    uint64_t nb;
+    bool has[7];
     if (dims == 3) {
       const uint64_t i = me / (k * k), j = (me / k) % k, l = me % k;
-      nb = (i > 0) + (i + 1 < k) + (j > 0) + (j + 1 < k) + (l > 0) + (l + 1 < k);
+      const bool h3[7] = {i > 0, j > 0, l > 0, true, l + 1 < k, j + 1 < k, i + 1 < k};
+      std::copy(h3, h3 + 7, has);
     } else {
       const uint64_t i = me / k, j = me % k;
-      nb = (i > 0) + (i + 1 < k) + (j > 0) + (j + 1 < k);
+      const bool h2[5] = {i > 0, j > 0, true, j + 1 < k, i + 1 < k};
+      std::copy(h2, h2 + 5, has);
     }
-    fro += diag * diag + (double)nb;
+    for (int q = 0; q < 2 * dims + 1; ++q)
+      if (has[q]) fro += op->coef[q] * op->coef[q];
   }
   op->a_fro_local2 = fro;
   *out = op;
   return BO_OK;
+}
+
+extern "C" int bo_op_laplace(bo_ctx ctx, int dims, uint64_t k, bo_op* out, bo_status* st) {
+  // problems.cpp:65-113: diagonal 2 * dims, every neighbour -1
+  const double c3[7] = {-1.0, -1.0, -1.0, 6.0, -1.0, -1.0, -1.0};
+  const double c2[5] = {-1.0, -1.0, 4.0, -1.0, -1.0};
+  return bo_op_stencil(ctx, dims, k, dims == 3 ? c3 : c2, out, st);
 }
 
 extern "C" int bo_op_destroy(bo_op op) {
@@ -688,19 +710,25 @@ int op_apply(bo_op op, const double* x, double* y, bo_status* st) {
   const int grid = (int)std::max<long long>(1, std::min<long long>((long long)ctx->num_sms * 8, (nl + 255) / 256));
   if (op->kind == 0)
     spmv_csr_kernel<<<grid, 256, 0, ctx->stream>>>(nl, op->row_ptr, op->col, op->val, xe, y);
-  else if (ctx->n_global + 2 * op->k * op->k < (1ull << 31) && op->k % 4 == 0 && ctx->row_begin % 4 == 0 &&
-           nl % 4 == 0 && op->halo_lo % 2 == 0 && ((uintptr_t)xe % 16) == 0 && ((uintptr_t)y % 16) == 0) {
-    const uint32_t ng = (uint32_t)(nl / 4);
-    const int g4 = (int)std::max<long long>(1, std::min<long long>((long long)ctx->num_sms * 8, (ng + 255) / 256));
-    spmv_laplace4_kernel<<<g4, 256, 0, ctx->stream>>>(op->dims, (uint32_t)op->k, (uint32_t)ctx->row_begin, ng,
-                                                     (uint32_t)op->halo_lo, xe, y);
-  } else if (ctx->n_global + 2 * op->k * op->k < (1ull << 31))
-    spmv_laplace_kernel<uint32_t><<<grid, 256, 0, ctx->stream>>>(op->dims, (uint32_t)op->k, (uint32_t)ctx->row_begin,
-                                                                 (uint32_t)nl, (uint32_t)op->halo_lo, xe, y);
-  else
-    spmv_laplace_kernel<unsigned long long><<<grid, 256, 0, ctx->stream>>>(
-        op->dims, (unsigned long long)op->k, (unsigned long long)ctx->row_begin, (unsigned long long)nl,
-        (unsigned long long)op->halo_lo, xe, y);
+  else {
+    Stencil stc;
+    for (int q = 0; q < 7; ++q) stc.c[q] = op->coef[q];
+    if (ctx->n_global + 2 * op->k * op->k < (1ull << 31) && op->k % 4 == 0 && ctx->row_begin % 4 == 0 &&
+        nl % 4 == 0 && op->halo_lo % 2 == 0 && ((uintptr_t)xe % 16) == 0 && ((uintptr_t)y % 16) == 0) {
+      const uint32_t ng = (uint32_t)(nl / 4);
+      const int g4 = (int)std::max<long long>(1, std::min<long long>((long long)ctx->num_sms * 8, (ng + 255) / 256));
+      spmv_stencil4_kernel<<<g4, 256, 0, ctx->stream>>>(op->dims, (uint32_t)op->k, (uint32_t)ctx->row_begin, ng,
+                                                        (uint32_t)op->halo_lo, stc, xe, y);
+    } else if (ctx->n_global + 2 * op->k * op->k < (1ull << 31)) {
+      spmv_stencil_kernel<uint32_t><<<grid, 256, 0, ctx->stream>>>(op->dims, (uint32_t)op->k,
+                                                                   (uint32_t)ctx->row_begin, (uint32_t)nl,
+                                                                   (uint32_t)op->halo_lo, stc, xe, y);
+    } else {
+      spmv_stencil_kernel<unsigned long long><<<grid, 256, 0, ctx->stream>>>(
+          op->dims, (unsigned long long)op->k, (unsigned long long)ctx->row_begin, (unsigned long long)nl,
+          (unsigned long long)op->halo_lo, stc, xe, y);
+    }
+  }
   CU(cudaGetLastError());
   ctx->launches++;
   return BO_OK;

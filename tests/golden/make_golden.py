@@ -22,8 +22,42 @@ sys.path.insert(0, str(ROOT / "oracle"))
 from py_oracle import Oracle  # noqa: E402
 
 
+def gmres_kat(res):
+    return {"converged": res.converged, "breakdown": res.breakdown, "detail": res.breakdown_detail,
+            "restarts": res.restarts, "iterations": res.iterations, "final_relres": res.final_relres,
+            "reduce": res.reduce, "reduce_total": res.reduce_total, "relres": res.relres,
+            "lsq": res.lsq}
+
+
+def extra_sections(r):
+    """Sections added after the first fixture (python make_golden.py --update):
+    the config-5 proxy (3D convection-diffusion 40^3, all four schemes) and the
+    full-size config-3 CholQR2 breakdown (laplace_3d(200), n = 8e6)."""
+    out = {}
+    sys.path.insert(0, str(ROOT))
+    from paper_2503_16717_b200.borth import convdiff_coeffs
+    csr = r.stencil_csr(40, 3, convdiff_coeffs(0.3))
+    n = 40 ** 3
+    out["gmres_convdiff40"] = {
+        name: gmres_kat(r.sstep_gmres(csr, np.ones(n), np.zeros(n), m=60, s=5, shat=60, scheme=scheme,
+                                      diagnostics=False))
+        for name, scheme in [("cholqr2", 0), ("randcholqr", 1), ("twostage_pip", 2), ("twostage_randbcgs", 3)]}
+    csr = r.laplace(200, 3)
+    n = 200 ** 3
+    out["gmres_c3_cholqr2"] = gmres_kat(r.sstep_gmres(csr, np.ones(n), np.zeros(n), m=60, s=10, shat=60, scheme=0,
+                                                      diagnostics=False))
+    return out
+
+
 def main():
     r = Oracle("ref")
+    path = Path(__file__).resolve().parent / "reference_kats.json"
+    if "--update" in sys.argv:
+        out = json.loads(path.read_text())
+        out.update(extra_sections(r))
+        path.write_text(json.dumps(out, indent=1))
+        print("updated", path)
+        return
     out = {"generator": "tests/golden/make_golden.py over oracle/_ref (reference sources, g++ -O3 -DNDEBUG)"}
     # --- rng (rng.hpp)
     out["derive_seed"] = {f"{b},{s}": str(r.derive_seed(b, s)) for b, s in [(0, 0), (0, 1), (7960286522194355700, 0),
@@ -118,7 +152,7 @@ def main():
     # --- spmv
     out["spmv_tridiag"] = r.spmv((np.array([0, 2, 5, 7]), np.array([0, 1, 0, 1, 2, 1, 2]),
                                   np.array([2.0, -1, -1, 2, -1, -1, 2])), np.ones(3)).tolist()
-    path = Path(__file__).resolve().parent / "reference_kats.json"
+    out.update(extra_sections(r))
     path.write_text(json.dumps(out, indent=1))
     print("wrote", path)
 

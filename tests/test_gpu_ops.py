@@ -1,5 +1,7 @@
 """GPU parity for the matrix-powers kernel, breakdown recovery, BCGS-PIP,
 RandBCGS / two-stage, and the s-step GMRES driver against the CPU oracle."""
+from pathlib import Path
+
 import numpy as np
 import pytest
 
@@ -282,3 +284,69 @@ def test_gmres_randcholqr_s10_converges(gpu, mk, orc):
     assert rep["restarts"] == want.restarts
     assert rep["iterations"] == want.iterations
     assert rep["reduce"] == want.reduce
+
+
+# ------------------------------------------- config 5 / config 3 (full size) --
+def _golden():
+    import json
+    return json.loads((Path(__file__).resolve().parent / "golden" / "reference_kats.json").read_text())
+
+
+@pytest.mark.parametrize("dims,k,coeffs", [(3, 20, "convdiff"), (3, 33, "convdiff"), (3, 40, "convdiff"),
+                                           (2, 100, [-0.5, -1.25, 4.5, -0.75, -2.0]), (2, 7, [1, 2, 3, 4, 5])])
+def test_stencil_spmv_bit_exact(gpu, mk, orc, dims, k, coeffs):
+    """matrix-free constant-coefficient stencil == CSR spmv (sparse.cpp:51-63)
+    on the from_triplets CSR of the same entries, bit for bit"""
+    c = gpu.borth.convdiff_coeffs(0.3) if coeffs == "convdiff" else np.asarray(coeffs, dtype=float)
+    csr = orc.csr_from_triplets(*orc.stencil_csr(k, dims, c))
+    n = len(csr[0]) - 1
+    ctx = mk(n)
+    x = np.random.default_rng(k).standard_normal(n)
+    want = orc.spmv(csr, x)
+    for op in (gpu.Operator.stencil(ctx, dims, k, c), gpu.Operator.csr(ctx, n, *csr)):
+        y = ctx.to_host(op.spmv(ctx.from_host(x)))[:, 0]
+        assert np.array_equal(y, want)
+    v = ctx.to_host(gpu.Operator.stencil(ctx, dims, k, c).mpk(ctx.from_host(x), 6))
+    assert np.array_equal(v, orc.mpk(csr, x, 6))
+
+
+@pytest.mark.parametrize("scheme", ["bcgs2_cholqr2", "bcgs2_randcholqr", "twostage_pip", "twostage_randbcgs"])
+def test_gmres_convdiff40(gpu, mk, scheme):
+    """Config-5 proxy: nonsymmetric 3D convection-diffusion 40^3,
+    s = 5, m = shat = 60, matrix-free stencil.  Against the reference's own run
+    (tests/golden): converged in 4 restarts / 240 iterations, identical ledger
+    (two-stage 57 reduces vs 233 one-stage), relres inside the envelope."""
+    want = _golden()["gmres_convdiff40"][scheme.replace("bcgs2_", "")]
+    n = 40 ** 3
+    ctx = mk(n)
+    op = gpu.Operator.convdiff(ctx, 40, 0.3)
+    x, rep = gpu.sstep_gmres_solve(op, ctx.from_host(np.ones(n)), ctx.from_host(np.zeros(n)), m=60, s=5, shat=60,
+                                   scheme=scheme, diagnostics=False)
+    assert rep["converged"] and want["converged"]
+    assert (rep["restarts"], rep["iterations"]) == (want["restarts"], want["iterations"]) == (4, 240)
+    assert rep["reduce"] == want["reduce"] and rep["reduce_total"] == want["reduce_total"]
+    # 10x the reference's own sensitivity on this problem (one-ulp changes of
+    # b move relres by 5.8e-14, 2.6e-11, 1.8e-9, 5.6e-8 at restarts 0-3,
+    # scripts/convdiff_envelope.py), floored at 1e-10
+    env = [1e-10, 2.6e-10, 1.8e-8, 5.6e-7]
+    for i, (g, w) in enumerate(zip(rep["restart_relres"], want["relres"])):
+        assert abs(g - w) <= env[i] * abs(w), (i, g, w)
+
+
+def test_gmres_c3_cholqr2_full_size(gpu, mk):
+    """Config 3 at full size (laplace_3d(200), n = 8e6, s = 10, m = 60):
+    bcgs2 + CholQR2 breaks down in panel 1 exactly as the reference does
+    (1 restart, 10 iterations, ledger 2/4/0/2, identical detail
+    string, relres 0.89544336171479355, LSQ residual 2532.696292920969)."""
+    want = _golden()["gmres_c3_cholqr2"]
+    n = 200 ** 3
+    ctx = mk(n)
+    op = gpu.Operator.laplace(ctx, 3, 200)
+    x, rep = gpu.sstep_gmres_solve(op, ctx.from_host(np.ones(n)), ctx.from_host(np.zeros(n)), m=60, s=10, shat=60,
+                                   scheme="bcgs2_cholqr2", diagnostics=False)
+    assert rep["breakdown"] and want["breakdown"] and not rep["converged"]
+    assert rep["breakdown_detail"] == want["detail"]
+    assert (rep["restarts"], rep["iterations"]) == (want["restarts"], want["iterations"]) == (1, 10)
+    assert rep["reduce"] == want["reduce"] == [2, 4, 0, 2]
+    assert abs(rep["final_relres"] - want["final_relres"]) <= 1e-10 * want["final_relres"]
+    assert abs(rep["restart_lsq_residual"][0] - want["lsq"][0]) <= 1e-8 * want["lsq"][0]

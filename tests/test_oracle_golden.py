@@ -121,3 +121,31 @@ def test_gmres_kats(orc, name):
     assert res.reduce == want["reduce"] and res.reduce_total == want["reduce_total"]
     assert res.relres == want["relres"]  # bit-identical histories
     assert res.final_relres == want["final_relres"]
+
+
+@pytest.mark.parametrize("name,scheme", [("cholqr2", 0), ("randcholqr", 1), ("twostage_pip", 2),
+                                         ("twostage_randbcgs", 3)])
+def test_gmres_convdiff40_kats(orc, name, scheme):
+    """config-5 proxy: the C oracle on the stencil CSR reproduces the
+    reference's histories bit for bit"""
+    import paper_2503_16717_b200.borth as B
+    want = G["gmres_convdiff40"][name]
+    csr = orc.stencil_csr(40, 3, B.convdiff_coeffs(0.3))
+    n = 40 ** 3
+    res = orc.sstep_gmres(csr, np.ones(n), np.zeros(n), m=60, s=5, shat=60, scheme=scheme, diagnostics=False)
+    assert (res.restarts, res.iterations) == (want["restarts"], want["iterations"])
+    assert res.reduce == want["reduce"]
+    assert res.relres == want["relres"]
+
+
+def test_stencil_csr_is_from_triplets_csr(orc):
+    """the test-side stencil generator emits exactly the CSR from_triplets
+    builds, and reproduces laplace_3d / laplace_2d (problems.cpp:65-113)"""
+    import paper_2503_16717_b200.borth as B
+    for k, dims, c in [(7, 3, B.convdiff_coeffs(0.3)), (9, 2, [-1, -2, 5, -3, -4])]:
+        csr = orc.stencil_csr(k, dims, c)
+        assert all(np.array_equal(a, b) for a, b in zip(csr, orc.csr_from_triplets(*csr)))
+    for k, dims in [(12, 3), (15, 2)]:
+        lap = orc.laplace(k, dims)
+        c = [-1.0] * dims + [2.0 * dims] + [-1.0] * dims
+        assert all(np.array_equal(a, b) for a, b in zip(lap, orc.stencil_csr(k, dims, c)))
