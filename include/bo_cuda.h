@@ -90,6 +90,28 @@ int bo_nccl_get_unique_id(void* out, bo_status* st);
 int bo_ctx_create(int device, int rank, int world, const void* nccl_id, uint64_t n_global,
                   uint64_t row_begin, uint64_t row_end, void* stream, bo_ctx* out,
                   bo_status* st);
+/* Host-provided collective transport (MPI, gloo, a serving runtime ...) in
+ * place of NCCL.  All buffers are device memory of this context; each call
+ * must be ordered after the work already queued on `stream` and complete
+ * (or be queued on `stream`) before it returns.  Return 0 on success. */
+typedef struct {
+  int peer;       /* rank */
+  int is_send;    /* 1 send buf to peer, 0 receive into buf from peer */
+  double* buf;
+  uint64_t count; /* doubles */
+} bo_p2p_op;
+typedef struct {
+  void* user;
+  /* in-place sum over all ranks of count doubles (the ledger's logical all-reduce) */
+  int (*allreduce_sum_f64)(void* user, double* buf, uint64_t count, void* stream);
+  /* recv[r * count + i] = send_r[i] for every rank r */
+  int (*allgather_u64)(void* user, const uint64_t* send, uint64_t count, uint64_t* recv, void* stream);
+  /* one group of point-to-point transfers (matrix-powers halo exchange) */
+  int (*exchange_f64)(void* user, int nops, const bo_p2p_op* ops, void* stream);
+} bo_comm_ops;
+/* as bo_ctx_create, with collectives through `comm` (copied) instead of NCCL */
+int bo_ctx_create_comm(int device, int rank, int world, const bo_comm_ops* comm, uint64_t n_global,
+                       uint64_t row_begin, uint64_t row_end, void* stream, bo_ctx* out, bo_status* st);
 int bo_ctx_destroy(bo_ctx ctx);
 int bo_ctx_synchronize(bo_ctx ctx, bo_status* st);
 uint64_t bo_ctx_local_rows(bo_ctx ctx);

@@ -46,6 +46,20 @@ class SolveReport(C.Structure):
     ]
 
 
+class P2pOp(C.Structure):
+    _fields_ = [("peer", C.c_int), ("is_send", C.c_int), ("buf", C.c_void_p), ("count", u64)]
+
+
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, u64, C.c_void_p)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, u64, C.c_void_p, C.c_void_p)
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.POINTER(P2pOp), C.c_void_p)
+
+
+class CommOps(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("allreduce_sum_f64", ALLREDUCE_FN), ("allgather_u64", ALLGATHER_FN),
+                ("exchange_f64", EXCHANGE_FN)]
+
+
 class ProfRecord(C.Structure):
     _fields_ = [("kind", C.c_int), ("k", C.c_int), ("p", C.c_int), ("mh", C.c_int), ("rows", u64),
                 ("bytes", u64), ("ms", C.c_float)]
@@ -59,6 +73,8 @@ _SIGS = {
     "bo_nccl_id_bytes": (C.c_int, []),
     "bo_nccl_get_unique_id": (C.c_int, [vp, SP]),
     "bo_ctx_create": (C.c_int, [C.c_int, C.c_int, C.c_int, vp, u64, u64, u64, vp, C.POINTER(vp), SP]),
+    "bo_ctx_create_comm": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(CommOps), u64, u64, u64, vp,
+                                     C.POINTER(vp), SP]),
     "bo_ctx_destroy": (C.c_int, [vp]),
     "bo_ctx_synchronize": (C.c_int, [vp, SP]),
     "bo_ctx_local_rows": (u64, [vp]),

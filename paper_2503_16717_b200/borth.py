@@ -150,13 +150,90 @@ def _ledger_out(led, arr):
         led.counts = list(arr)
 
 
+# -------------------------------------------------------------- transport --
+class TorchDistComm:
+    """Collective transport through an initialised torch.distributed process
+    group (e.g. gloo) for bo_ctx_create_comm: device buffers are staged
+    through host memory.  Used to run the sharded (world > 1) path of the
+    library on one GPU in tests; production multi-GPU runs use NCCL."""
+
+    def __init__(self, group=None):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist, self.group = torch, dist, group
+        self.ops = L.CommOps(None, L.ALLREDUCE_FN(self._allreduce), L.ALLGATHER_FN(self._allgather),
+                             L.EXCHANGE_FN(self._exchange))
+        self.calls = {"allreduce": 0, "allgather": 0, "exchange": 0}
+
+    def _view(self, ptr, count, dtype):
+        t = self.torch
+        class _H:  # noqa: E306
+            __cuda_array_interface__ = {"shape": (int(count),), "typestr": "<f8" if dtype == "f8" else "<i8",
+                                        "data": (int(ptr), False), "version": 3, "strides": None}
+        return t.as_tensor(_H(), device="cuda")
+
+    def _sync(self, stream):
+        self.torch.cuda.ExternalStream(int(stream)).synchronize()
+
+    def _allreduce(self, user, buf, count, stream):
+        try:
+            self._sync(stream)
+            dev = self._view(buf, count, "f8")
+            host = dev.cpu()
+            self.dist.all_reduce(host, group=self.group)
+            dev.copy_(host)
+            self.torch.cuda.synchronize()
+            self.calls["allreduce"] += 1
+            return 0
+        except Exception:  # pragma: no cover - reported as BO_NCCL by the library
+            return 1
+
+    def _allgather(self, user, send, count, recv, stream):
+        try:
+            self._sync(stream)
+            mine = self._view(send, count, "i8").cpu()
+            parts = [self.torch.empty_like(mine) for _ in range(self.dist.get_world_size(self.group))]
+            self.dist.all_gather(parts, mine, group=self.group)
+            out = self._view(recv, count * len(parts), "i8")
+            out.copy_(self.torch.cat(parts).to(out.device))
+            self.torch.cuda.synchronize()
+            self.calls["allgather"] += 1
+            return 0
+        except Exception:  # pragma: no cover
+            return 1
+
+    def _exchange(self, user, nops, ops, stream):
+        try:
+            self._sync(stream)
+            reqs, recvs = [], []
+            for i in range(nops):
+                o = ops[i]
+                dev = self._view(o.buf, o.count, "f8")
+                if o.is_send:
+                    h = dev.cpu()
+                    reqs.append(self.dist.isend(h, o.peer, group=self.group))
+                else:
+                    h = self.torch.empty(int(o.count), dtype=self.torch.float64)
+                    reqs.append(self.dist.irecv(h, o.peer, group=self.group))
+                    recvs.append((dev, h))
+            for r in reqs:
+                r.wait()
+            for dev, h in recvs:
+                dev.copy_(h)
+            self.torch.cuda.synchronize()
+            self.calls["exchange"] += 1
+            return 0
+        except Exception:  # pragma: no cover
+            return 1
+
+
 # ---------------------------------------------------------------- context --
 class Context:
     """One GPU: the row shard [row_begin, row_end) of an n-row problem."""
 
     def __init__(self, n: int, *, device: int = 0, rank: int = 0, world: int = 1,
                  row_begin: int | None = None, row_end: int | None = None,
-                 nccl_id: bytes | None = None, stream=None):
+                 nccl_id: bytes | None = None, stream=None, comm=None):
         import torch
         self.lib = L.load()
         self.torch = torch
@@ -174,9 +251,14 @@ class Context:
         # it (from_host, panel) is issued on the same stream
         self.stream = stream if stream is not None else torch.cuda.Stream(self.device)
         h = C.c_void_p()
-        idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
-        _call(self.lib.bo_ctx_create, device, rank, world, idbuf, n, row_begin, row_end,
-              C.c_void_p(self.stream.cuda_stream), C.byref(h))
+        self._comm = comm  # keeps the ctypes callbacks alive
+        if comm is not None:
+            _call(self.lib.bo_ctx_create_comm, device, rank, world, C.byref(comm.ops), n, row_begin, row_end,
+                  C.c_void_p(self.stream.cuda_stream), C.byref(h))
+        else:
+            idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+            _call(self.lib.bo_ctx_create, device, rank, world, idbuf, n, row_begin, row_end,
+                  C.c_void_p(self.stream.cuda_stream), C.byref(h))
         self.h = h
         self.n_local = int(self.lib.bo_ctx_local_rows(h))
         self.ld = int(self.lib.bo_ctx_ld(h))

@@ -350,13 +350,8 @@ int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st) {
     ctx->prof.push_back({r.kind, r.K, r.p, mh, rows, bytes, pe0, pe1});
   }
   if (ctx->world > 1) {
-    NcclApi& nc = nccl();
-    int rc = nc.AllReduce(ctx->sums, ctx->sums, (size_t)a.part_len, kNcclFloat64, kNcclSum, ctx->nccl,
-                          ctx->stream);
-    if (rc != 0)
-      return set_st(st, BO_NCCL, 0, 0.0, "ncclAllReduce failed: %s",
-                    nc.GetErrorString ? nc.GetErrorString(rc) : "?");
-    ctx->allreduces++;
+    // one all-reduce per pass that reduces (a ledger event); store-only passes have none
+    if (ki.qtx || ki.gram || ki.sk != SK_NONE) TRY(comm_allreduce(ctx, ctx->sums, (size_t)a.part_len, st));
     if (f.ops) {
       finalize_kernel<<<1, 256, 0, ctx->stream>>>(f);
       CU(cudaGetLastError());
@@ -410,6 +405,49 @@ int run_pass(bo_ctx ctx, PassReq& r, bo_status* st) {
 }
 
 // zero the device status word
+// ---------------------------------------------------------------------------
+// collective transport
+// ---------------------------------------------------------------------------
+int comm_allreduce(bo_ctx ctx, double* buf, size_t n, bo_status* st) {
+  ctx->allreduces++;
+  if (ctx->has_comm) {
+    const int rc = ctx->comm.allreduce_sum_f64(ctx->comm.user, buf, n, ctx->stream);
+    return rc ? set_st(st, BO_NCCL, rc, 0.0, "all-reduce callback failed (%d)", rc) : BO_OK;
+  }
+  NcclApi& nc = nccl();
+  const int rc = nc.AllReduce(buf, buf, n, kNcclFloat64, kNcclSum, ctx->nccl, ctx->stream);
+  return rc ? set_st(st, BO_NCCL, rc, 0.0, "ncclAllReduce failed: %s", nc.GetErrorString ? nc.GetErrorString(rc) : "?")
+            : BO_OK;
+}
+int comm_allgather_u64(bo_ctx ctx, const uint64_t* send, size_t n, uint64_t* recv, bo_status* st) {
+  if (ctx->has_comm) {
+    const int rc = ctx->comm.allgather_u64(ctx->comm.user, send, n, recv, ctx->stream);
+    return rc ? set_st(st, BO_NCCL, rc, 0.0, "all-gather callback failed (%d)", rc) : BO_OK;
+  }
+  NcclApi& nc = nccl();
+  if (!nc.AllGather) return set_st(st, BO_NCCL, 0, 0.0, "ncclAllGather missing");
+  const int rc = nc.AllGather(send, recv, n, kNcclUint64, ctx->nccl, ctx->stream);
+  return rc ? set_st(st, BO_NCCL, rc, 0.0, "ncclAllGather failed (%d)", rc) : BO_OK;
+}
+int comm_exchange(bo_ctx ctx, int nops, const bo_p2p_op* ops, bo_status* st) {
+  if (nops == 0) return BO_OK;
+  if (ctx->has_comm) {
+    const int rc = ctx->comm.exchange_f64(ctx->comm.user, nops, ops, ctx->stream);
+    return rc ? set_st(st, BO_NCCL, rc, 0.0, "exchange callback failed (%d)", rc) : BO_OK;
+  }
+  NcclApi& nc = nccl();
+  if (!nc.Send || !nc.Recv || !nc.GroupStart || !nc.GroupEnd) return set_st(st, BO_NCCL, 0, 0.0, "NCCL p2p missing");
+  nc.GroupStart();
+  for (int i = 0; i < nops; ++i) {
+    if (ops[i].is_send)
+      nc.Send(ops[i].buf, ops[i].count, kNcclFloat64, ops[i].peer, ctx->nccl, ctx->stream);
+    else
+      nc.Recv(ops[i].buf, ops[i].count, kNcclFloat64, ops[i].peer, ctx->nccl, ctx->stream);
+  }
+  const int rc = nc.GroupEnd();
+  return rc ? set_st(st, BO_NCCL, rc, 0.0, "NCCL group send/recv failed (%d)", rc) : BO_OK;
+}
+
 int reset_status(bo_ctx ctx, bo_status* st) {
   CU(cudaMemsetAsync(ctx->status, 0, sizeof(DevStatus), ctx->stream));
   return BO_OK;
@@ -477,9 +515,24 @@ extern "C" int bo_nccl_get_unique_id(void* out, bo_status* st) {
   return BO_OK;
 }
 
+static int ctx_create_impl(int device, int rank, int world, const void* nccl_id, const bo_comm_ops* comm,
+                           uint64_t n_global, uint64_t row_begin, uint64_t row_end, void* stream, bo_ctx* out,
+                           bo_status* st);
 extern "C" int bo_ctx_create(int device, int rank, int world, const void* nccl_id, uint64_t n_global,
                              uint64_t row_begin, uint64_t row_end, void* stream, bo_ctx* out,
                              bo_status* st) {
+  return ctx_create_impl(device, rank, world, nccl_id, nullptr, n_global, row_begin, row_end, stream, out, st);
+}
+extern "C" int bo_ctx_create_comm(int device, int rank, int world, const bo_comm_ops* comm, uint64_t n_global,
+                                  uint64_t row_begin, uint64_t row_end, void* stream, bo_ctx* out, bo_status* st) {
+  ok_st(st);
+  if (!comm || !comm->allreduce_sum_f64 || !comm->allgather_u64 || !comm->exchange_f64)
+    return set_st(st, BO_INVALID, 0, 0.0, "bo_comm_ops needs allreduce_sum_f64, allgather_u64 and exchange_f64");
+  return ctx_create_impl(device, rank, world, nullptr, comm, n_global, row_begin, row_end, stream, out, st);
+}
+static int ctx_create_impl(int device, int rank, int world, const void* nccl_id, const bo_comm_ops* comm,
+                           uint64_t n_global, uint64_t row_begin, uint64_t row_end, void* stream, bo_ctx* out,
+                           bo_status* st) {
   ok_st(st);
   *out = nullptr;
   int ndev = 0;
@@ -524,7 +577,10 @@ extern "C" int bo_ctx_create(int device, int rank, int world, const void* nccl_i
     CU(cudaMalloc(&c->scratch[i], c->ld * 16 * 8));
     CU(cudaMemset(c->scratch[i], 0, c->ld * 16 * 8));
   }
-  if (world > 1) {
+  if (comm) {
+    c->has_comm = true;
+    c->comm = *comm;
+  } else if (world > 1) {
     NcclApi& nc = nccl();
     if (!nc.ok) {
       bo_ctx_destroy(c);

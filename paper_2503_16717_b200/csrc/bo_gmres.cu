@@ -153,11 +153,8 @@ int reduce_sum(Gm& g, int nparts, double* out, bo_status* st) {
   double s = 0.0;
   for (int i = 0; i < nparts; ++i) s += g.hpart[i];
   if (ctx->world > 1) {
-    CU(cudaMemcpy(g.gsum, &s, 8, cudaMemcpyHostToDevice));
-    NcclApi& nc = nccl();
-    int rc = nc.AllReduce(g.gsum, g.gsum, 1, kNcclFloat64, kNcclSum, ctx->nccl, ctx->stream);
-    if (rc) return set_st(st, BO_NCCL, 0, 0.0, "ncclAllReduce failed (%d)", rc);
-    ctx->allreduces++;
+    CU(cudaMemcpyAsync(g.gsum, &s, 8, cudaMemcpyHostToDevice, ctx->stream));
+    TRY(comm_allreduce(ctx, g.gsum, 1, st));
     CU(cudaMemcpyAsync(&s, g.gsum, 8, cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
   }
@@ -464,9 +461,9 @@ extern "C" int bo_sstep_gmres(bo_op op, const double* b, const double* x0, const
   // ||A||_F (gmres.cpp:286-288)
   double a_fro2 = op->a_fro_local2;
   if (ctx->world > 1) {
-    CU(cudaMemcpy(g.gsum, &a_fro2, 8, cudaMemcpyHostToDevice));
-    int rc = nccl().AllReduce(g.gsum, g.gsum, 1, kNcclFloat64, kNcclSum, ctx->nccl, ctx->stream);
-    if (rc) return set_st(st, BO_NCCL, 0, 0.0, "ncclAllReduce failed (%d)", rc);
+    CU(cudaMemcpyAsync(g.gsum, &a_fro2, 8, cudaMemcpyHostToDevice, ctx->stream));
+    TRY(comm_allreduce(ctx, g.gsum, 1, st));
+    ctx->allreduces--;  // setup, not a ledger event
     CU(cudaMemcpyAsync(&a_fro2, g.gsum, 8, cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
   }

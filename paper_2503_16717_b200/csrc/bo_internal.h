@@ -15,6 +15,8 @@ struct bo_ctx_s {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   void* nccl = nullptr;  // ncclComm_t
+  bool has_comm = false;  // collectives through host callbacks (bo_ctx_create_comm)
+  bo_comm_ops comm{};
   uint64_t n_global = 0, row_begin = 0, row_end = 0, n_local = 0, ld = 0;
   int num_sms = 0;
   size_t smem_optin = 0;
@@ -216,6 +218,10 @@ int sketch_pass(bo_sketch sk, const double* v, uint64_t ldv, int K, int pass_id,
 void push_panel_host(bo_basis b, uint64_t k, const double* proj, uint64_t ldp, const double* diag, uint64_t ldd,
                      bool overlap);
 uint64_t derive_seed(uint64_t base, uint64_t stream);
+// the context's collective transport (NCCL, or bo_comm_ops callbacks)
+int comm_allreduce(bo_ctx ctx, double* buf, size_t n, bo_status* st);
+int comm_allgather_u64(bo_ctx ctx, const uint64_t* send, size_t n, uint64_t* recv, bo_status* st);
+int comm_exchange(bo_ctx ctx, int nops, const bo_p2p_op* ops, bo_status* st);
 int op_apply(bo_op op, const double* x, double* y, bo_status* st);
 int sketch_to_host(bo_sketch th, const double* v, uint64_t ldv, int K, std::vector<double>& S, bo_status* st);
 inline uint64_t round_up(uint64_t x, uint64_t m) { return (x + m - 1) / m * m; }

@@ -363,10 +363,7 @@ int wide_contract(bo_ctx ctx, const double* L, uint64_t ldl, int ml, const doubl
   CU(cudaGetLastError());
   ctx->launches++;
   if (ctx->world > 1) {
-    NcclApi& nc = nccl();
-    int rc = nc.AllReduce(ctx->sums, ctx->sums, 4096, kNcclFloat64, kNcclSum, ctx->nccl, ctx->stream);
-    if (rc) return set_st(st, BO_NCCL, 0, 0.0, "ncclAllReduce failed (%d)", rc);
-    ctx->allreduces++;
+    TRY(comm_allreduce(ctx, ctx->sums, 4096, st));
   }
   std::vector<double> h(4096);
   CU(cudaMemcpyAsync(h.data(), ctx->sums, 4096 * 8, cudaMemcpyDeviceToHost, ctx->stream));
@@ -538,14 +535,11 @@ int op_setup_halo(bo_op op, long long need_lo, long long need_hi, bo_status* st)
   op->halo_hi = (uint64_t)std::max<long long>(0, need_hi - (long long)ctx->row_end);
   if (ctx->world > 1) {
     // every rank learns its neighbours' needs: [halo_lo, halo_hi] per rank
-    NcclApi& nc = nccl();
-    if (!nc.AllGather || !nc.Send || !nc.Recv) return set_st(st, BO_NCCL, 0, 0.0, "NCCL p2p symbols missing");
     uint64_t* d = nullptr;
     CU(cudaMalloc(&d, (2 + 2 * ctx->world) * 8));
     uint64_t mine[2] = {op->halo_lo, op->halo_hi};
     CU(cudaMemcpy(d, mine, 16, cudaMemcpyHostToDevice));
-    int rc = nc.AllGather(d, d + 2, 2, kNcclUint64, ctx->nccl, ctx->stream);
-    if (rc) return set_st(st, BO_NCCL, 0, 0.0, "ncclAllGather failed (%d)", rc);
+    TRY(comm_allgather_u64(ctx, d, 2, d + 2, st));
     std::vector<uint64_t> all(2 * ctx->world);
     CU(cudaMemcpyAsync(all.data(), d + 2, 16 * ctx->world, cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
@@ -570,21 +564,19 @@ int halo_exchange(bo_op op, const double* x, const double** xe, bo_status* st) {
   }
   CU(cudaMemcpyAsync(op->xext + op->halo_lo, x, ctx->n_local * 8, cudaMemcpyDeviceToDevice, ctx->stream));
   if (ctx->world > 1) {
-    NcclApi& nc = nccl();
-    nc.GroupStart();
+    bo_p2p_op ops[4];
+    int n = 0;
     const int r = ctx->rank;
+    double* xs = const_cast<double*>(x);
     if (r > 0) {
-      if (op->halo_lo) nc.Recv(op->xext, op->halo_lo, kNcclFloat64, r - 1, ctx->nccl, ctx->stream);
-      if (op->peer_need_hi) nc.Send(x, op->peer_need_hi, kNcclFloat64, r - 1, ctx->nccl, ctx->stream);
+      if (op->halo_lo) ops[n++] = {r - 1, 0, op->xext, op->halo_lo};
+      if (op->peer_need_hi) ops[n++] = {r - 1, 1, xs, op->peer_need_hi};
     }
     if (r + 1 < ctx->world) {
-      if (op->halo_hi)
-        nc.Recv(op->xext + op->halo_lo + ctx->n_local, op->halo_hi, kNcclFloat64, r + 1, ctx->nccl, ctx->stream);
-      if (op->peer_need_lo)
-        nc.Send(x + ctx->n_local - op->peer_need_lo, op->peer_need_lo, kNcclFloat64, r + 1, ctx->nccl, ctx->stream);
+      if (op->halo_hi) ops[n++] = {r + 1, 0, op->xext + op->halo_lo + ctx->n_local, op->halo_hi};
+      if (op->peer_need_lo) ops[n++] = {r + 1, 1, xs + ctx->n_local - op->peer_need_lo, op->peer_need_lo};
     }
-    int rc = nc.GroupEnd();
-    if (rc) return set_st(st, BO_NCCL, 0, 0.0, "halo exchange failed (%d)", rc);
+    TRY(comm_exchange(ctx, n, ops, st));
   }
   *xe = op->xext;
   return BO_OK;
