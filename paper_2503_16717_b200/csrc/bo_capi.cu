@@ -339,7 +339,7 @@ int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st) {
     TRY(make_tmap(&tmT, ki.sk == SK_GAUSS ? r.sk->theta : nullptr, ctx->n_local, mh,
                   ki.sk == SK_GAUSS ? r.sk->ldth : 0, S, st));
   }
-  fn<<<grid, (consumer_warps(ki.upd) + 1) * 32, total, ctx->stream>>>(a, tmV, tmQ, tmT);
+  fn<<<grid, pass_threads(ki.upd), total, ctx->stream>>>(a, tmV, tmQ, tmT);
   CU(cudaGetLastError());
   ctx->launches++;
   if (ctx->profiling) {

@@ -259,7 +259,7 @@ __device__ __forceinline__ void row_trsm_n(double (&x)[NR][kMaxK], const double*
 // the number of 8-column tiles is dispatched to a compile-time constant.
 template <int NT, int T, int NPRE, bool UPD, int NPOST, bool QTX, bool GRAM, int SK, bool STORE, bool EXACT,
           int KC = 0>
-__global__ void __launch_bounds__((consumer_warps(UPD) + 1) * 32, 1)
+__global__ void __launch_bounds__(pass_threads(UPD), 1)
     pass_kernel(const __grid_constant__ PassArgs a, const __grid_constant__ CUtensorMap tmV,
                 const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmT) {
   constexpr int S = TileGeom<T>::S;
@@ -312,7 +312,8 @@ __global__ void __launch_bounds__((consumer_warps(UPD) + 1) * 32, 1)
     s_skip = a.status->code != ST_OK;
     for (int s = 0; s < NS; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], ROWG ? 1 : NW);
+      if (BO_PRODUCER_WARP) ptx::mbar_init(&empty[s], ROWG ? 1 : NW);
+      else reinterpret_cast<unsigned*>(&empty[s])[0] = 0u;  // arrival counter
     }
     ptx::fence_mbar_init();
   }
@@ -371,7 +372,60 @@ __global__ void __launch_bounds__((consumer_warps(UPD) + 1) * 32, 1)
       use = it / NS;
     }
   };
-  if (warp == NW) {
+  auto issue = [&](int it, int s) {
+    const long long row0 = (long long)(blockIdx.x + (long long)it * gridDim.x) * T;
+    const long long valid = nrows - row0 < T ? nrows - row0 : T;
+    const uint32_t cb = (SK == SK_COUNT) ? (uint32_t)(((valid + 3) & ~3LL) * 4) : 0u;
+    double* st = stages + (size_t)s * L.stage;
+    ptx::mbar_arrive_expect_tx(&full[s], box_bytes + cb);
+    ptx::tma_load_2d(st + L.offV, &tmV, (int)row0, 0, &full[s]);
+    if (ncolQ) ptx::tma_load_2d(st + L.offQ, &tmQ, (int)row0, 0, &full[s]);
+    if (ncolT) ptx::tma_load_2d(st + L.offT, &tmT, (int)row0, 0, &full[s]);
+    if (SK == SK_COUNT) ptx::bulk_g2s(st + L.offC, a.code + row0, cb, &full[s]);
+  };
+  // A consumer warp calls release(it, s) after its last read of stage s for
+  // tile it.  With a producer warp that is an mbarrier arrival; otherwise the
+  // last warp to release a stage refills it with the tile NS ahead (row mode:
+  // the owning warp refills its private ring), so no warp ever waits to issue.
+  unsigned* arrivals = reinterpret_cast<unsigned*>(empty);
+  auto release = [&](int it, int s) {
+    __syncwarp();
+    if (lane == 0) {
+      if (BO_PRODUCER_WARP) {
+        ptx::mbar_arrive(&empty[s]);
+      } else if (ROWG) {
+        if (it + NW * nsub < my_tiles) {
+          ptx::fence_proxy_async_smem();  // our generic-proxy reads before the async-proxy refill
+          issue(it + NW * nsub, s);
+        }
+      } else {
+        __threadfence_block();
+        if (atomicAdd(reinterpret_cast<unsigned*>(&empty[s]), 1u) == (unsigned)(NW - 1)) {
+          reinterpret_cast<unsigned*>(&empty[s])[0] = 0u;
+          __threadfence_block();
+          if (it + NS < my_tiles) {
+            ptx::fence_proxy_async_smem();
+            issue(it + NS, s);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  };
+  (void)arrivals;
+  if (!BO_PRODUCER_WARP) {
+    if (ROWG ? lane == 0 : tid == 0) {
+      ptx::prefetch_tmap(&tmV);
+      if (ncolQ) ptx::prefetch_tmap(&tmQ);
+      if (ncolT) ptx::prefetch_tmap(&tmT);
+      if (ROWG) {
+        for (int j = 0; j < nsub && warp + NW * j < my_tiles; ++j) issue(warp + NW * j, warp + NW * j);
+      } else {
+        for (int it = 0; it < NS && it < my_tiles; ++it) issue(it, it);
+      }
+    }
+  }
+  if (BO_PRODUCER_WARP && warp == NW) {
     if (lane == 0) {
       ptx::prefetch_tmap(&tmV);
       if (ncolQ) ptx::prefetch_tmap(&tmQ);
@@ -379,16 +433,8 @@ __global__ void __launch_bounds__((consumer_warps(UPD) + 1) * 32, 1)
       for (int it = 0; it < my_tiles; ++it) {
         int s, use;
         stage_of(it, s, use);
-        const long long row0 = (long long)(blockIdx.x + (long long)it * gridDim.x) * T;
-        const long long valid = nrows - row0 < T ? nrows - row0 : T;
-        const uint32_t cb = (SK == SK_COUNT) ? (uint32_t)(((valid + 3) & ~3LL) * 4) : 0u;
         if (use > 0) ptx::mbar_wait(&empty[s], (use - 1) & 1);
-        double* st = stages + (size_t)s * L.stage;
-        ptx::mbar_arrive_expect_tx(&full[s], box_bytes + cb);
-        ptx::tma_load_2d(st + L.offV, &tmV, (int)row0, 0, &full[s]);
-        if (ncolQ) ptx::tma_load_2d(st + L.offQ, &tmQ, (int)row0, 0, &full[s]);
-        if (ncolT) ptx::tma_load_2d(st + L.offT, &tmT, (int)row0, 0, &full[s]);
-        if (SK == SK_COUNT) ptx::bulk_g2s(st + L.offC, a.code + row0, cb, &full[s]);
+        issue(it, s);
       }
     }
   } else {
@@ -462,8 +508,7 @@ __global__ void __launch_bounds__((consumer_warps(UPD) + 1) * 32, 1)
             }
           }
         }
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&empty[s]);
+        release(it, s);
       }
       // warp butterfly (fixed order) of every Gram entry
 #pragma unroll
@@ -508,8 +553,7 @@ __global__ void __launch_bounds__((consumer_warps(UPD) + 1) * 32, 1)
             }
           }
         }
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&empty[s]);
+        release(it, s);
         ptx::named_bar_arrive(2 + b, NW * 32);  // X buffer b full
       }
       for (int it = (my_tiles >= 2 ? my_tiles - 2 : 0); it < my_tiles; ++it)
@@ -693,8 +737,7 @@ __global__ void __launch_bounds__((consumer_warps(UPD) + 1) * 32, 1)
             }
           }
         }
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&empty[s]);
+        release(it, s);
         if (SPLIT) {
           if (STORE && gtid < K) ptx::bulk_wait_read0();
           ptx::named_bar_arrive(4 + b, NW * 32);  // X buffer b may be refilled
