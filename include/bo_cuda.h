@@ -47,7 +47,9 @@ typedef enum {
   BO_INVALID = 6,                /* errors.hpp:71 InvalidScheme / bad arguments */
   BO_ZERO_MATRIX = 7,            /* errors.hpp:65 ZeroMatrix */
   BO_CUDA = 8,                   /* CUDA runtime failure / no GPU */
-  BO_NCCL = 9                    /* NCCL failure */
+  BO_NCCL = 9,                   /* NCCL / collective transport failure */
+  BO_PARSE_ERROR = 10,           /* errors.hpp:77 ParseError (MatrixMarket) */
+  BO_BANNER_ERROR = 11           /* errors.hpp:88 BannerError (MatrixMarket) */
 } bo_code;
 
 typedef struct {
@@ -242,6 +244,19 @@ int bo_op_laplace(bo_ctx ctx, int dims, uint64_t k, bo_op* out, bo_status* st);
  * reference, SURVEY finding 4) is coeffs = (-1-w, -1-w, -1-w, 6, -1+w, -1+w, -1+w). */
 int bo_op_stencil(bo_ctx ctx, int dims, uint64_t k, const double* coeffs, bo_op* out, bo_status* st);
 int bo_op_destroy(bo_op op);
+/* MatrixMarket ingestion (sparse.cpp:88-136 read_matrix_market, :138-152
+ * write_matrix_market): "matrix coordinate real general|symmetric"; the CSR
+ * is what CsrMatrix::from_triplets builds (sorted, duplicates summed,
+ * symmetric entries mirrored).  Errors: BO_PARSE_ERROR / BO_BANNER_ERROR with
+ * the reference what() text.  Host-only: no GPU needed.  Feed the rows of a
+ * shard to bo_op_csr. */
+typedef struct bo_csr_host_s* bo_csr_host;
+int bo_mm_read(const char* path, bo_csr_host* out, bo_status* st);
+int bo_csr_host_info(bo_csr_host h, uint64_t* nrows, uint64_t* ncols, uint64_t* nnz);
+int bo_csr_host_arrays(bo_csr_host h, int64_t* row_ptr, int64_t* col, double* val);
+int bo_csr_host_destroy(bo_csr_host h);
+int bo_mm_write(const char* path, uint64_t nrows, uint64_t ncols, const int64_t* row_ptr, const int64_t* col,
+                const double* val, bo_status* st);
 /* spmv (sparse.cpp:51-63): y = A x (local rows; x is the local shard, halo
  * exchanged internally when world > 1) */
 int bo_spmv(bo_op op, const double* x, double* y, bo_status* st);

@@ -332,6 +332,24 @@ void* ref_csr_from_triplets(size_t nr, size_t nc, size_t nt, const size_t* r, co
   for (size_t i = 0; i < nt; ++i) t[i] = {r[i], c[i], v[i]};
   return new RefCsr{CsrMatrix::from_triplets(nr, nc, std::move(t))};
 }
+/* read_matrix_market (sparse.cpp:88-136): NULL + message on a thrown Error */
+void* ref_mm_read(const char* path, char* msg, size_t msg_len) {
+  try {
+    return new RefCsr{read_matrix_market(path)};
+  } catch (const Error& e) {
+    std::snprintf(msg, msg_len, "%s", e.what());
+    return nullptr;
+  }
+}
+int ref_mm_write(const char* path, void* a, char* msg, size_t msg_len) {
+  try {
+    write_matrix_market(path, static_cast<RefCsr*>(a)->a);
+    return 0;
+  } catch (const Error& e) {
+    std::snprintf(msg, msg_len, "%s", e.what());
+    return 1;
+  }
+}
 void ref_csr_free(void* a) { delete static_cast<RefCsr*>(a); }
 size_t ref_csr_info(void* a, size_t* nrows, size_t* ncols) {
   const CsrMatrix& m = static_cast<RefCsr*>(a)->a;

@@ -129,6 +129,11 @@ _SIGS = {
     "bo_op_laplace": (C.c_int, [vp, C.c_int, u64, C.POINTER(vp), SP]),
     "bo_op_stencil": (C.c_int, [vp, C.c_int, u64, dp, C.POINTER(vp), SP]),
     "bo_op_destroy": (C.c_int, [vp]),
+    "bo_mm_read": (C.c_int, [C.c_char_p, C.POINTER(vp), SP]),
+    "bo_csr_host_info": (C.c_int, [vp, u64p, u64p, u64p]),
+    "bo_csr_host_arrays": (C.c_int, [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64), dp]),
+    "bo_csr_host_destroy": (C.c_int, [vp]),
+    "bo_mm_write": (C.c_int, [C.c_char_p, u64, u64, C.POINTER(C.c_int64), C.POINTER(C.c_int64), dp, SP]),
     "bo_spmv": (C.c_int, [vp, vp, vp, SP]),
     "bo_mpk": (C.c_int, [vp, vp, u64, vp, u64, SP]),
     "bo_sstep_gmres": (C.c_int, [vp, vp, vp, C.POINTER(SolverConfig), vp, C.POINTER(SolveReport), SP]),

@@ -72,6 +72,17 @@ class ZeroMatrix(Error):
     pass
 
 
+class ParseError(Error):
+    """errors.hpp:77 (MatrixMarket); .line = offending line number"""
+    def __init__(self, msg, line):
+        super().__init__(msg)
+        self.line = line
+
+
+class BannerError(Error):
+    """errors.hpp:88 (MatrixMarket banner)"""
+
+
 class CudaError(RuntimeError):
     pass
 
@@ -100,6 +111,10 @@ def _raise(rc: int, st: L.Status):
         raise CudaError(msg)
     if rc == 9:
         raise NcclError(msg)
+    if rc == 10:
+        raise ParseError(msg, int(st.index))
+    if rc == 11:
+        raise BannerError(msg)
     raise Error(f"bo error {rc}: {msg}")
 
 
@@ -655,6 +670,37 @@ def two_stage_cycle(store: BasisStore, panels, preproc, theta=None, reorthogonal
     for v in panels:
         two_stage_panel(store, v, preproc, theta, overlap)
     return two_stage_finish(store, preproc, reorthogonalize, record_condition)
+
+
+# --------------------------------------------------------- MatrixMarket --
+def read_matrix_market(path) -> tuple:
+    """read_matrix_market (sparse.cpp:88-136): (nrows, ncols, row_ptr, col, val)
+    of the CSR CsrMatrix::from_triplets builds; raises ParseError / BannerError
+    with the reference's messages.  Host-only."""
+    lib = L.load()
+    h = C.c_void_p()
+    _call(lib.bo_mm_read, str(path).encode(), C.byref(h))
+    try:
+        nr, nc, nnz = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        lib.bo_csr_host_info(h, C.byref(nr), C.byref(nc), C.byref(nnz))
+        rp = np.zeros(nr.value + 1, dtype=np.int64)
+        ci = np.zeros(nnz.value, dtype=np.int64)
+        vv = np.zeros(nnz.value)
+        lib.bo_csr_host_arrays(h, rp.ctypes.data_as(C.POINTER(C.c_int64)), ci.ctypes.data_as(C.POINTER(C.c_int64)),
+                               _dp(vv))
+    finally:
+        lib.bo_csr_host_destroy(h)
+    return nr.value, nc.value, rp, ci, vv
+
+
+def write_matrix_market(path, nrows: int, ncols: int, row_ptr, col, val):
+    """write_matrix_market (sparse.cpp:138-152)"""
+    lib = L.load()
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(col, dtype=np.int64)
+    vv = np.ascontiguousarray(val, dtype=np.float64)
+    _call(lib.bo_mm_write, str(path).encode(), nrows, ncols, rp.ctypes.data_as(C.POINTER(C.c_int64)),
+          ci.ctypes.data_as(C.POINTER(C.c_int64)), _dp(vv))
 
 
 # -------------------------------------------------------------- operator --

@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
   constexpr int NG = ROWG ? KC * (KC + 1) / 2 : 1;
   static_assert(!(QTX && UPD), "a pass either projects or updates");
   static_assert(!STORE || XT, "stores come from the X tile");
-  static_assert(!SPLIT || T <= GAW * 64, "row-solve group handles two rows per thread");
+  static_assert(!SPLIT || T <= GAW * 128, "row-solve group handles at most four rows per thread");
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;

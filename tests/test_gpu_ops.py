@@ -350,3 +350,23 @@ def test_gmres_c3_cholqr2_full_size(gpu, mk):
     assert rep["reduce"] == want["reduce"] == [2, 4, 0, 2]
     assert abs(rep["final_relres"] - want["final_relres"]) <= 1e-10 * want["final_relres"]
     assert abs(rep["restart_lsq_residual"][0] - want["lsq"][0]) <= 1e-8 * want["lsq"][0]
+
+
+def test_gmres_c1_from_matrix_market(gpu, mk, orc, tmp_path):
+    """ingestion end to end: laplace_2d(100) through write/read_matrix_market
+    (sparse.cpp:88-152) into the CSR operator, then config 1 with CholQR2:
+    the reference's restart / iteration counts, ledger and relres history"""
+    want = _golden()["gmres_2d100"]["c1_cholqr2"]
+    rp, ci, vv = orc.laplace(100, 2)
+    n = len(rp) - 1
+    gpu.borth.write_matrix_market(tmp_path / "lap.mtx", n, n, rp, ci, vv)
+    nr, nc, rp2, ci2, vv2 = gpu.borth.read_matrix_market(tmp_path / "lap.mtx")
+    assert (nr, nc) == (n, n) and np.array_equal(rp2, rp) and np.array_equal(ci2, ci) and np.array_equal(vv2, vv)
+    ctx = mk(n)
+    op = gpu.Operator.csr(ctx, nc, rp2, ci2, vv2)
+    x, rep = gpu.sstep_gmres_solve(op, ctx.from_host(np.ones(n)), ctx.from_host(np.zeros(n)), m=60, s=5, shat=60,
+                                   scheme="bcgs2_cholqr2", diagnostics=False)
+    assert rep["converged"] and (rep["restarts"], rep["iterations"]) == (want["restarts"], want["iterations"])
+    assert rep["reduce"] == want["reduce"]
+    for i, (g, w) in enumerate(zip(rep["restart_relres"], want["relres"])):
+        assert abs(g - w) <= _envelope(i) * abs(w), (i, g, w)

@@ -95,3 +95,95 @@ def test_count_rows_from_jumped_window(lib, orc):
             u, sg = draws[2 * t], draws[2 * t + 1]
             assert (u * width) >> 64 == bo[a + t]
             assert (1.0 if sg & 1 else -1.0) == so[a + t]
+
+
+# ------------------------------------------------------------ MatrixMarket --
+MM_CASES = {
+    "general": "%%MatrixMarket matrix coordinate real general\n% comment\n\n3 4 5\n1 1 2.5\n3 4 -1e-3\n2 2 7\n"
+               "1 3 0.125\n3 1 1e300\n",
+    "symmetric": "%%MatrixMarket matrix coordinate real symmetric\n4 4 5\n1 1 4\n2 1 -1\n3 2 -1\n4 4 4\n4 3 -0.5\n",
+    "duplicates": "%%MatrixMarket matrix coordinate real general\n2 2 5\n1 2 0.1\n1 2 0.2\n2 1 3\n1 2 0.3\n2 2 1\n",
+    "upper_banner": "%%MatrixMarket MATRIX Coordinate REAL General\n2 2 1\n2 2 1.5\n",
+    "empty_rows": "%%MatrixMarket matrix coordinate real general\n5 5 2\n5 1 1\n1 5 2\n",
+    "bad_banner": "%%MatrixMarket matrix array real general\n2 2\n1\n2\n3\n4\n",
+    "complex": "%%MatrixMarket matrix coordinate complex general\n1 1 1\n1 1 1 0\n",
+    "not_mm": "hello\n",
+    "bad_size": "%%MatrixMarket matrix coordinate real general\n3 x 1\n",
+    "bad_entry": "%%MatrixMarket matrix coordinate real general\n3 3 1\n1 two 3\n",
+    "out_of_range": "%%MatrixMarket matrix coordinate real general\n3 3 2\n1 1 1\n4 1 1\n",
+    "no_size": "%%MatrixMarket matrix coordinate real general\n% only comments\n",
+    "empty": "",
+}
+
+
+def _ref_mm(ref, path):
+    import ctypes as C
+    f = ref.lib.ref_mm_read
+    f.restype, f.argtypes = C.c_void_p, [C.c_char_p, C.c_char_p, C.c_size_t]
+    msg = C.create_string_buffer(512)
+    h = f(str(path).encode(), msg, 512)
+    if not h:
+        return None, msg.value.decode()
+    nr, nc = C.c_size_t(), C.c_size_t()
+    ref.lib.ref_csr_info.restype = C.c_size_t
+    ref.lib.ref_csr_info.argtypes = [C.c_void_p, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]
+    nnz = ref.lib.ref_csr_info(h, C.byref(nr), C.byref(nc))
+    rp = np.zeros(nr.value + 1, dtype=np.uint64)
+    ci = np.zeros(nnz, dtype=np.uint64)
+    vv = np.zeros(nnz)
+    ref.lib.ref_csr_arrays.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                                       C.POINTER(C.c_double)]
+    ref.lib.ref_csr_arrays(h, rp.ctypes.data_as(C.POINTER(C.c_uint64)), ci.ctypes.data_as(C.POINTER(C.c_uint64)),
+                           vv.ctypes.data_as(C.POINTER(C.c_double)))
+    ref.lib.ref_csr_free.argtypes = [C.c_void_p]
+    ref.lib.ref_csr_free(h)
+    return (nr.value, nc.value, rp.astype(np.int64), ci.astype(np.int64), vv), None
+
+
+@pytest.mark.parametrize("case", sorted(MM_CASES))
+def test_matrix_market_read_matches_reference(ref, tmp_path, case):
+    """bo_mm_read == the reference's read_matrix_market (sparse.cpp:88-136):
+    identical CSR (sorted, symmetric mirrored, duplicates summed) or the
+    identical error text"""
+    import paper_2503_16717_b200 as P
+    path = tmp_path / f"{case}.mtx"
+    path.write_text(MM_CASES[case])
+    want, err = _ref_mm(ref, path)
+    if want is None:
+        with pytest.raises(P.borth.Error) as ex:
+            P.borth.read_matrix_market(path)
+        assert str(ex.value) == err
+        assert isinstance(ex.value, P.borth.ParseError if err.startswith("parse error") else P.borth.BannerError)
+        return
+    got = P.borth.read_matrix_market(path)
+    assert got[:2] == want[:2]
+    for a, b in zip(got[2:], want[2:]):
+        assert np.array_equal(a, b)
+
+
+def test_matrix_market_missing_file(ref, tmp_path):
+    import paper_2503_16717_b200 as P
+    _, err = _ref_mm(ref, tmp_path / "nope.mtx")
+    with pytest.raises(P.borth.ParseError) as ex:
+        P.borth.read_matrix_market(tmp_path / "nope.mtx")
+    assert str(ex.value) == err and ex.value.line == 0
+
+
+def test_matrix_market_write_matches_reference(ref, orc, tmp_path):
+    """bo_mm_write == write_matrix_market byte for byte, and round-trips"""
+    import ctypes as C
+
+    import paper_2503_16717_b200 as P
+    rp, ci, vv = orc.stencil_csr(6, 3, P.borth.convdiff_coeffs(0.3))
+    vv = vv * np.pi  # 17-digit values
+    n = len(rp) - 1
+    P.borth.write_matrix_market(tmp_path / "ours.mtx", n, n, rp, ci, vv)
+    h, keep = ref._csr_handle(rp, ci, vv, n)
+    f = ref.lib.ref_mm_write
+    f.restype, f.argtypes = C.c_int, [C.c_char_p, C.c_void_p, C.c_char_p, C.c_size_t]
+    msg = C.create_string_buffer(256)
+    assert f(str(tmp_path / "ref.mtx").encode(), h, msg, 256) == 0
+    ref._csr_free(h)
+    assert (tmp_path / "ours.mtx").read_bytes() == (tmp_path / "ref.mtx").read_bytes()
+    got = P.borth.read_matrix_market(tmp_path / "ours.mtx")
+    assert np.array_equal(got[2], rp) and np.array_equal(got[3], ci) and np.array_equal(got[4], vv)
