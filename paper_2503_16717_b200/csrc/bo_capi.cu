@@ -152,7 +152,11 @@ PassFn get_pass_fn(int nt, int T, int kind, bool exact, int K) {
   const KindInfo& ki = kKindInfo[kind];
   if (ki.npre > 0 || ki.npost > 0) {
     PassFn f = nullptr;
-    if (T == 128) {
+    if (T == 256) {
+      if (K == 6) f = pass_fn_kc6_t256(kind);
+      if (K == 11) f = pass_fn_kc11_t256(kind);
+      if (K == 16) f = pass_fn_kc16_t256(kind);
+    } else if (T == 128) {
       if (K == 6) f = pass_fn_kc6_t128(kind);
       if (K == 11) f = pass_fn_kc11_t128(kind);
       if (K == 16) f = pass_fn_kc16_t128(kind);
@@ -163,8 +167,8 @@ PassFn get_pass_fn(int nt, int T, int kind, bool exact, int K) {
     }
     if (f) return f;
   }
-  if (nt == 1) return T == 128 ? pass_fn_nt1_t128(kind) : pass_fn_nt1_t64(kind);
-  return T == 128 ? pass_fn_nt2_t128(kind) : pass_fn_nt2_t64(kind);
+  if (nt == 1) return T == 256 ? pass_fn_nt1_t256(kind) : T == 128 ? pass_fn_nt1_t128(kind) : pass_fn_nt1_t64(kind);
+  return T == 256 ? pass_fn_nt2_t256(kind) : T == 128 ? pass_fn_nt2_t128(kind) : pass_fn_nt2_t64(kind);
 }
 
 // launch one streaming pass (+ its reduction / finalize) on the ctx stream
@@ -212,41 +216,48 @@ int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st) {
 
   const int nt = r.K <= 8 ? 1 : 2;
   const size_t avail = std::min<size_t>(ctx->smem_optin, 227 * 1024) - 1024;  // static smem headroom
-  // Tile choice: maximise the bytes the producer can keep in flight
-  // ((NS-1) stages, Little's law against ~1-2 us HBM latency), prefer T=128.
+  // Tile choice: the largest tile (256 / 128 / 64 rows) whose stage ring is
+  // at least double-buffered.  Per-tile synchronisation costs ~0.3-1 us
+  // (ncu + T = 64 vs 128 sweeps), so larger tiles amortise it; the row-mode
+  // Gram (ROWG) needs 128-row tiles; BO_TILE forces a size.
   static const int tile_env = [] {
     const char* e = getenv("BO_TILE");
     return e ? atoi(e) : 0;
   }();
+  static const int tile_max = [] {
+    const char* e = getenv("BO_MAX_TILE");
+    return e ? atoi(e) : 256;
+  }();
+  const bool rowg_kind = !r.exact && ki.npre > 0 && ki.gram && !ki.qtx && !ki.upd && ki.sk == SK_NONE &&
+                         !ki.store && ki.npost == 0 && (r.K == 6 || r.K == 11);
   int T = 0, NS = 0;
   size_t region0 = 0, total = 0;
-  for (int tt : {128, 64}) {
-    if (r.exact && tt != 64) continue;
-    if (tile_env && tt != tile_env) continue;
-    const int S = tt + 4;
-    // row-mode Gram (bo_pass.cuh ROWG): unpadded stages, no X tile
-    const bool rowg = !r.exact && ki.npre > 0 && ki.gram && !ki.qtx && !ki.upd && ki.sk == SK_NONE && !ki.store &&
-                      ki.npost == 0 && (r.K == 6 || r.K == 11) && tt == 128;
-    const StageLayout SL = stage_layout(r.K, (ki.qtx || ki.upd) ? r.p : 0, ki.sk == SK_GAUSS ? mh : 0,
-                                        ki.sk == SK_COUNT, tt, !rowg);
-    const size_t stage = (size_t)SL.stage * 8;
-    const bool xt = (ki.npre > 0 || ki.upd || ki.npost > 0) && !rowg;
-    // row-major copies of the solve factors (bo_pass.cuh RFT) in K-specialised solve passes
-    const bool rft = !r.exact && (ki.npre > 0 || ki.npost > 0) && (r.K == 6 || r.K == 11 || r.K == 16);
-    const size_t fixed = (xt ? 2 * (size_t)nt * 8 * S * 8 : 0) + (3 * 256 + 48 + (rft ? 3 * 256 : 0)) * 8 +
-                         (ki.sk == SK_COUNT ? (size_t)mh * r.K * 8 : 0) + 2 * kMaxStages * 8;
-    const size_t need_red = (size_t)consumer_warps(ki.upd) * dm_len * 8;
-    const size_t need_fin = (512 + (size_t)std::max(mh, 1) * 16 + 64) * 8;
-    if (avail <= fixed) continue;
-    int ns = (int)std::min<size_t>(kMaxStages, (avail - fixed) / stage);
-    if (rowg) ns = ns / consumer_warps(false) * consumer_warps(false);  // one private sub-ring per warp
-    if (ns < 1) continue;
-    const size_t r0 = round_up(std::max({(size_t)ns * stage, need_red, need_fin}), 128);
-    if (r0 + fixed > avail) continue;
-    // Prefer the 128-row tile (fewer barriers per byte; measured faster at
-    // every pass shape) whenever it double-buffers; else the deeper 64-row ring.
-    const bool better = T == 0 || (ns >= 2 && NS < 2);
-    if (better) {
+  for (int want_ns : {2, 1}) {
+    for (int tt : {256, 128, 64}) {
+      if (T) break;
+      if (r.exact && tt != 64) continue;
+      if (tile_env && tt != tile_env) continue;
+      if (tt > tile_max) continue;
+      if (rowg_kind && tt != 128 && !tile_env) continue;
+      const int S = tile_stride(tt), nsub = tt / tile_sub_rows(tt);
+      // row-mode Gram (bo_pass.cuh ROWG): unpadded stages, no X tile
+      const bool rowg = rowg_kind && tt == 128;
+      const StageLayout SL = stage_layout(r.K, (ki.qtx || ki.upd) ? r.p : 0, ki.sk == SK_GAUSS ? mh : 0,
+                                          ki.sk == SK_COUNT, tt, !rowg);
+      const size_t stage = (size_t)SL.stage * 8;
+      const bool xt = (ki.npre > 0 || ki.upd || ki.npost > 0) && !rowg;
+      // row-major copies of the solve factors (bo_pass.cuh RFT) in K-specialised solve passes
+      const bool rft = !r.exact && (ki.npre > 0 || ki.npost > 0) && (r.K == 6 || r.K == 11 || r.K == 16);
+      const size_t fixed = (xt ? 2 * (size_t)nt * 8 * S * 8 * nsub : 0) + (3 * 256 + 48 + (rft ? 3 * 256 : 0)) * 8 +
+                           (ki.sk == SK_COUNT ? (size_t)mh * r.K * 8 : 0) + 2 * kMaxStages * 8;
+      const size_t need_red = (size_t)consumer_warps(ki.upd) * dm_len * 8;
+      const size_t need_fin = (512 + (size_t)std::max(mh, 1) * 16 + 64) * 8;
+      if (avail <= fixed) continue;
+      int ns = (int)std::min<size_t>(kMaxStages, (avail - fixed) / stage);
+      if (rowg) ns = ns / consumer_warps(false) * consumer_warps(false);  // one private sub-ring per warp
+      if (ns < want_ns) continue;
+      const size_t r0 = round_up(std::max({(size_t)ns * stage, need_red, need_fin}), 128);
+      if (r0 + fixed > avail) continue;
       T = tt;
       NS = ns;
       region0 = r0;
@@ -333,7 +344,7 @@ int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st) {
   }
   CUtensorMap tmV, tmQ, tmT;
   {
-    const int S = T + 4;
+    const int S = tile_stride(T);
     TRY(make_tmap(&tmV, r.V, ctx->n_local, r.K, r.ldv, S, st));
     TRY(make_tmap(&tmQ, (ki.qtx || ki.upd) ? r.Q : nullptr, ctx->n_local, r.p, r.ldq, S, st));
     TRY(make_tmap(&tmT, ki.sk == SK_GAUSS ? r.sk->theta : nullptr, ctx->n_local, mh,

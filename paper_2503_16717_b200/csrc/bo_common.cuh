@@ -31,21 +31,36 @@ __host__ __device__ constexpr int pass_threads(bool upd) { return (consumer_warp
 constexpr int kMaxConsumerWarps = BO_NW_UPD > BO_NW_OTHER ? BO_NW_UPD : BO_NW_OTHER;
 constexpr int kMaxStages = 24;   // shared-memory stage ring depth bound
 
-// Shared-memory stage layout (doubles): every operand block starts on a
-// 128-byte boundary (TMA destination alignment); column stride S = T + 4.
+// Tile geometry.  A tile of T rows is staged as T / R sub-tiles of R <= 128
+// rows; within a sub-tile an operand block is column-major with the padded
+// column stride S = R + 4 (conflict-free DMMA fragment loads), and the
+// sub-tiles of one operand block follow each other.  Element (c, r) of a block
+// of P columns sits at (r / R) * P * S + c * S + r % R.  Every sub-tile is one
+// 2-D TMA box of S rows, so one tensor map serves every T.
+template <int T>
+struct TileGeom {
+  static constexpr int R = T < 128 ? T : 128;
+  static constexpr int NSUB = T / R;
+  static constexpr int S = R + 4;
+};
+__host__ __device__ inline int tile_sub_rows(int T) { return T < 128 ? T : 128; }
+__host__ __device__ inline int tile_stride(int T) { return tile_sub_rows(T) + 4; }
+
 struct StageLayout {
   int offV, offQ, offT, offC, stage;
 };
 __host__ __device__ inline int ru16(int x) { return (x + 15) & ~15; }
+// Shared-memory stage layout (doubles): every operand block starts on a
+// 128-byte boundary (TMA destination alignment).
 // pad: operand blocks hold a multiple of 8 columns (zero padding for the MMA
 // tiles); row-mode passes (no tensor-core reads) pack the columns tightly.
 __host__ __device__ inline StageLayout stage_layout(int K, int ncolQ, int ncolT, bool count, int T, bool pad = true) {
-  const int S = T + 4;
+  const int S = tile_stride(T), nsub = T / tile_sub_rows(T);
   StageLayout L;
   L.offV = 0;
-  L.offQ = ru16((pad ? ((K + 7) & ~7) : K) * S);
-  L.offT = L.offQ + ru16(((ncolQ + 7) & ~7) * S);
-  L.offC = L.offT + ru16(((ncolT + 7) & ~7) * S);
+  L.offQ = ru16((pad ? ((K + 7) & ~7) : K) * S * nsub);
+  L.offT = L.offQ + ru16(((ncolQ + 7) & ~7) * S * nsub);
+  L.offC = L.offT + ru16(((ncolT + 7) & ~7) * S * nsub);
   L.stage = L.offC + (count ? ru16(T / 2) : 0);
   return L;
 }

@@ -35,10 +35,6 @@
 
 namespace bo {
 
-template <int T>
-struct TileGeom {
-  static constexpr int S = T + 4;  // padded column stride (doubles): conflict-free DMMA fragments
-};
 
 // ---------------------------------------------------------------------------
 // finalize (one CTA): the tiny factorizations after a reduction
@@ -263,6 +259,7 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
     pass_kernel(const __grid_constant__ PassArgs a, const __grid_constant__ CUtensorMap tmV,
                 const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmT) {
   constexpr int S = TileGeom<T>::S;
+  constexpr int NSUB = TileGeom<T>::NSUB;  // 128-row sub-tiles per tile (T = 256: 2)
   constexpr int NW = consumer_warps(UPD);
   constexpr bool SPLIT = NPRE > 0;
   constexpr int GAW = SPLIT ? BO_GAW : 0;  // row-solve warps (one per SM sub-partition: one row per thread)
@@ -294,11 +291,13 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
 
   const int ncolQ = (QTX || UPD) ? p : 0, ncolT = (SK == SK_GAUSS) ? mh : 0;
   const int mq = (ncolQ + 7) >> 3, ms = (ncolT + 7) >> 3;  // 8-column tiles
+  // offset of row r of a P-column operand block (see TileGeom): c * S + so(r, P)
+  auto so = [](int r, int P) { return NSUB > 1 ? (r >> 7) * P * S + (r & 127) : r; };
   const StageLayout L = stage_layout(K, ncolQ, ncolT, SK == SK_COUNT, T, !ROWG);
   const int NS = a.nstages;
   double* stages = reinterpret_cast<double*>(smem_raw);
-  double* xtile = stages + a.region0_dbl;                         // [2][KP][S]
-  double* rfac = xtile + ((XT && !ROWG) ? 2 * KP * S : 0);        // [3][256]
+  double* xtile = stages + a.region0_dbl;                         // [2][NSUB][KP][S]
+  double* rfac = xtile + ((XT && !ROWG) ? 2 * NSUB * KP * S : 0); // [3][256]
   double* rinv = rfac + 3 * 256;                                  // [3][16]
   constexpr bool RFT = KC > 0 && !EXACT && (NPRE > 0 || NPOST > 0);
   double* rft = rinv + 48;                                        // [3][256] row-major R, 1/r_jj on the diagonal
@@ -326,14 +325,15 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
   if (SK == SK_COUNT)
     for (int e = tid; e < mh * K; e += blockDim.x) cacc[e] = 0.0;
   // zero padding columns (never written by TMA or the phases)
-  for (int s = 0; s < (ROWG ? 0 : NS); ++s) {
-    double* st = stages + (size_t)s * L.stage;
-    for (int e = tid; e < (KP - K) * S; e += blockDim.x) st[L.offV + K * S + e] = 0.0;
-    for (int e = tid; e < (mq * 8 - ncolQ) * S; e += blockDim.x) st[L.offQ + ncolQ * S + e] = 0.0;
-    for (int e = tid; e < (ms * 8 - ncolT) * S; e += blockDim.x) st[L.offT + ncolT * S + e] = 0.0;
-  }
+  for (int s = 0; s < (ROWG ? 0 : NS); ++s)
+    for (int q = 0; q < NSUB; ++q) {
+      double* st = stages + (size_t)s * L.stage;
+      for (int e = tid; e < (KP - K) * S; e += blockDim.x) st[L.offV + q * KP * S + K * S + e] = 0.0;
+      for (int e = tid; e < (mq * 8 - ncolQ) * S; e += blockDim.x) st[L.offQ + q * mq * 8 * S + ncolQ * S + e] = 0.0;
+      for (int e = tid; e < (ms * 8 - ncolT) * S; e += blockDim.x) st[L.offT + q * ms * 8 * S + ncolT * S + e] = 0.0;
+    }
   if (XT && !ROWG)
-    for (int b = 0; b < 2; ++b)
+    for (int b = 0; b < 2 * NSUB; ++b)
       for (int e = tid; e < (KP - K) * S; e += blockDim.x) xtile[b * KP * S + K * S + e] = 0.0;
   __syncthreads();
   if (tid < 48) {
@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
   // Row mode: consumer warp w owns the stages w, w + NW, ... (NS / NW of
   // them) and its tiles w, w + NW, ... are loaded into them in order (a
   // private ring per warp: no phase aliasing between warps running apart).
-  const uint32_t box_bytes = (uint32_t)(S * 8 * (K + ncolQ + ncolT));
+  const uint32_t box_bytes = (uint32_t)(NSUB * S * 8 * (K + ncolQ + ncolT));
   const int nsub = ROWG ? NS / NW : NS;
   auto stage_of = [&](int it, int& s, int& use) {
     if (ROWG) {
@@ -378,9 +378,12 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
     const uint32_t cb = (SK == SK_COUNT) ? (uint32_t)(((valid + 3) & ~3LL) * 4) : 0u;
     double* st = stages + (size_t)s * L.stage;
     ptx::mbar_arrive_expect_tx(&full[s], box_bytes + cb);
-    ptx::tma_load_2d(st + L.offV, &tmV, (int)row0, 0, &full[s]);
-    if (ncolQ) ptx::tma_load_2d(st + L.offQ, &tmQ, (int)row0, 0, &full[s]);
-    if (ncolT) ptx::tma_load_2d(st + L.offT, &tmT, (int)row0, 0, &full[s]);
+#pragma unroll
+    for (int q = 0; q < NSUB; ++q) {
+      ptx::tma_load_2d(st + L.offV + q * KP * S, &tmV, (int)row0 + 128 * q, 0, &full[s]);
+      if (ncolQ) ptx::tma_load_2d(st + L.offQ + q * mq * 8 * S, &tmQ, (int)row0 + 128 * q, 0, &full[s]);
+      if (ncolT) ptx::tma_load_2d(st + L.offT + q * ms * 8 * S, &tmT, (int)row0 + 128 * q, 0, &full[s]);
+    }
     if (SK == SK_COUNT) ptx::bulk_g2s(st + L.offC, a.code + row0, cb, &full[s]);
   };
   // A consumer warp calls release(it, s) after its last read of stage s for
@@ -523,7 +526,7 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
         const long long row0 = (long long)(blockIdx.x + (long long)it * gridDim.x) * T;
         const int valid = (int)(nrows - row0 < T ? nrows - row0 : T);
         const double* stV = stages + (size_t)s * L.stage + L.offV;
-        double* xt = xtile + b * KP * S;
+        double* xt = xtile + b * NSUB * KP * S;
         ptx::mbar_wait(&full[s], (it / NS) & 1);
         if (it >= 2) ptx::named_bar_sync(4 + b, NW * 32);  // X buffer b drained by the U/S/R group
         {
@@ -534,7 +537,7 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
           for (int q = 0; q < RPT; ++q) {
             const int r = tid + q * GAWX * 32;
 #pragma unroll
-            for (int c = 0; c < kMaxK; ++c) x[q][c] = (c < K && r < T) ? stV[c * S + r] : 0.0;
+            for (int c = 0; c < kMaxK; ++c) x[q][c] = (c < K && r < T) ? stV[c * S + so(r, KP)] : 0.0;
           }
           if constexpr (KC > 0 && !EXACT) {
             row_trsm_t<KC, RPT>(x, rft);
@@ -549,7 +552,7 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
             if (r < T) {
 #pragma unroll
               for (int c = 0; c < kMaxK; ++c)
-                if (c < K) xt[c * S + r] = (r < valid) ? x[q][c] : 0.0;
+                if (c < K) xt[c * S + so(r, KP)] = (r < valid) ? x[q][c] : 0.0;
             }
           }
         }
@@ -569,7 +572,7 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
         const double* stQ = st + L.offQ;
         const double* stT = st + L.offT;
         const uint32_t* stC = reinterpret_cast<const uint32_t*>(st + L.offC);
-        double* xt = xtile + b * KP * S;
+        double* xt = xtile + b * NSUB * KP * S;
 
         if (!SPLIT && STORE && gtid < K) ptx::bulk_wait_read0();  // previous tile's store drained
         ptx::mbar_wait(&full[s], (it / NS) & 1);
@@ -585,12 +588,12 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
               const int r = rg * 8 + g;
               double av[2 * MQc > 0 ? 2 * MQc : 1];
 #pragma unroll
-              for (int ks = 0; ks < 2 * MQc; ++ks) av[ks] = stQ[(ks * 4 + t4) * S + r];
+              for (int ks = 0; ks < 2 * MQc; ++ks) av[ks] = stQ[(ks * 4 + t4) * S + so(r, mq * 8)];
               double d[NT][2];
 #pragma unroll
               for (int nj = 0; nj < NT; ++nj)
 #pragma unroll
-                for (int e = 0; e < 2; ++e) d[nj][e] = x0[(nj * 8 + 2 * t4 + e) * S + r];
+                for (int e = 0; e < 2; ++e) d[nj][e] = x0[(nj * 8 + 2 * t4 + e) * S + so(r, KP)];
 #pragma unroll
               for (int ks = 0; ks < 2 * MQc; ++ks)
 #pragma unroll
@@ -598,7 +601,7 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
 #pragma unroll
               for (int nj = 0; nj < NT; ++nj)
 #pragma unroll
-                for (int e = 0; e < 2; ++e) xt[(nj * 8 + 2 * t4 + e) * S + r] = d[nj][e];
+                for (int e = 0; e < 2; ++e) xt[(nj * 8 + 2 * t4 + e) * S + so(r, KP)] = d[nj][e];
             }
           };
           switch (mq) {
@@ -620,14 +623,14 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
           for (int r = gtid; r < T; r += GT) {
             double x[1][kMaxK];
 #pragma unroll
-            for (int c = 0; c < kMaxK; ++c) x[0][c] = (c < K) ? xt[c * S + r] : 0.0;
+            for (int c = 0; c < kMaxK; ++c) x[0][c] = (c < K) ? xt[c * S + so(r, KP)] : 0.0;
             if constexpr (KC > 0 && !EXACT)
               row_trsm_t<KC, 1>(x, rft + 512);
             else
               row_trsm<EXACT, KC>(x[0], rfac + 512, rinv + 32, K);
 #pragma unroll
             for (int c = 0; c < kMaxK; ++c)
-              if (c < K) xt[c * S + r] = (r < valid) ? x[0][c] : 0.0;
+              if (c < K) xt[c * S + so(r, KP)] = (r < valid) ? x[0][c] : 0.0;
           }
           ptx::named_bar_sync(GBAR, GT);
         }
@@ -637,8 +640,13 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
         // ---- S: bulk store of the X tile (one request per column)
         if (STORE && gtid < K) {
           ptx::fence_proxy_async_smem();
-          ptx::bulk_s2g(a.out + (long long)gtid * a.ldo + row0, xt + gtid * S,
-                        (uint32_t)(((valid + 1) & ~1) * 8));
+#pragma unroll
+          for (int q = 0; q < NSUB; ++q) {
+            const int vq = valid - 128 * q;
+            if (vq > 0)
+              ptx::bulk_s2g(a.out + (long long)gtid * a.ldo + row0 + 128 * q, xt + q * KP * S + gtid * S,
+                            (uint32_t)((((vq < 128 ? vq : 128) + 1) & ~1) * 8));
+          }
           ptx::bulk_commit();
         }
 
@@ -654,14 +662,14 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
               constexpr int slot = decltype(slot_c)::value;  // register-resident fragment sets
               const int r = ks * 4 + t4;
 #pragma unroll
-              for (int nj = 0; nj < NT; ++nj) bx[slot][nj] = X[(nj * 8 + g) * S + r];
+              for (int nj = 0; nj < NT; ++nj) bx[slot][nj] = X[(nj * 8 + g) * S + so(r, KP)];
               if (QTX) {
 #pragma unroll
-                for (int mi = 0; mi < MQc; ++mi) aq[slot][mi] = stQ[(mi * 8 + g) * S + r];
+                for (int mi = 0; mi < MQc; ++mi) aq[slot][mi] = stQ[(mi * 8 + g) * S + so(r, mq * 8)];
               }
               if (SK == SK_GAUSS) {
 #pragma unroll
-                for (int mi = 0; mi < MSc; ++mi) at[slot][mi] = stT[(mi * 8 + g) * S + r];
+                for (int mi = 0; mi < MSc; ++mi) at[slot][mi] = stT[(mi * 8 + g) * S + so(r, ms * 8)];
               }
             };
             auto mma = [&](auto slot_c) {
@@ -732,7 +740,7 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
                 const int rq = g32 * 32 + q;
                 const double sg = (stC[rq] & 0x80000000u) ? -1.0 : 1.0;
                 for (int c = 0; c < K; ++c)
-                  cacc[bk + c * mh] = tiny::add(cacc[bk + c * mh], tiny::mul(sg, X[c * S + rq]));
+                  cacc[bk + c * mh] = tiny::add(cacc[bk + c * mh], tiny::mul(sg, X[c * S + so(rq, KP)]));
               }
             }
           }

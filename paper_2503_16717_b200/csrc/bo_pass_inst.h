@@ -9,6 +9,11 @@
 namespace bo {
 namespace host {
 typedef void (*PassFn)(const PassArgs, const CUtensorMap, const CUtensorMap, const CUtensorMap);
+PassFn pass_fn_nt1_t256(int kind);
+PassFn pass_fn_nt2_t256(int kind);
+PassFn pass_fn_kc6_t256(int kind);
+PassFn pass_fn_kc11_t256(int kind);
+PassFn pass_fn_kc16_t256(int kind);
 PassFn pass_fn_nt1_t128(int kind);
 PassFn pass_fn_nt1_t64(int kind);
 PassFn pass_fn_nt2_t128(int kind);

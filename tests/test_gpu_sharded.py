@@ -151,7 +151,8 @@ def test_sharded_gmres(gpu, tmp_path, case):
     assert r["converged"]
     assert [r["restarts"], r["iterations"], r["reduce"]] == r["want"]
     # the single-GPU envelopes (tests/test_gpu_ops.py): 10x the reference's
-    # own reorder / libm sensitivity on each problem
-    env = ([1e-10] * 6 + [1e-8, 1e-6, 2e-3, 2e-3]) if case == "gmres_c1" else [1e-10, 2.6e-10, 1.8e-8, 5.6e-7]
+    # own sensitivity on each problem
+    from test_gpu_ops import C1_ENVELOPE
+    env = C1_ENVELOPE if case == "gmres_c1" else [1e-10, 2.6e-10, 1.8e-8, 5.6e-7]
     for i, (g, w) in enumerate(zip(r["relres"], r["want_relres"])):
         assert abs(g - w) <= env[i] * abs(w), (i, g, w)
