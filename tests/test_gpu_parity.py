@@ -335,3 +335,98 @@ def test_project_range(gpu, mk, orc):
     assert np.max(np.abs(pr.coeffs - co)) < 1e-13 * scale
     assert np.max(np.abs(ctx.to_host(pr.vhat) - vh)) < 1e-13 * scale
     assert st.ledger().counts == orc.basis_ledger(ob)
+
+
+# ----------------------------------------------- config 4: stability sweep --
+@pytest.mark.parametrize("w", [5, 10, 15])
+@pytest.mark.parametrize("kappa", [1e0, 1e4, 1e8, 1e12, 1e15])
+def test_c4_glued_stability_sweep(gpu, mk, orc, w, kappa):
+    """Config 4: 12 glued panels of width w with panel and
+    global condition kappa.  RandCholQR (Gaussian sketch) must complete every
+    panel with O(eps) orthogonality, like the reference; CholQR2 must complete
+    or break down in the same panel with the same ledger and message as the
+    reference (the failing step may move within the rounding-noise band where
+    the reference's own pivot sits at the floor)."""
+    n, panels = 10000, 12
+    v = orc.gen_glued(n, panels, w, kappa, kappa, 11)
+    ctx = mk(n)
+    th = gpu.SketchOperator.build(ctx, "gaussian", n, w - 1, 17)
+    oth = orc.sketch_build(0, n, w - 1, 17).h
+
+    def oracle_run(vv, intra):
+        ob = orc.basis_new(n, panels * w)
+        done, msg = 0, ""
+        for p in range(panels):
+            r = orc.bcgs2(ob, vv[:, p * w:(p + 1) * w], intra, oth if intra else None)
+            if r.code:
+                msg = r.msg
+                break
+            done += 1
+        led = orc.basis_ledger(ob)
+        orc.basis_free(ob)
+        return done, msg, led
+
+    # the reference's outcome is noise-determined when one-ulp changes of the
+    # input move it (failing pivot at the eps * max-diag floor)
+    vp = v.copy()
+    idx = np.random.default_rng(1).integers(0, n, 64)
+    vp[idx, 0] = np.nextafter(vp[idx, 0], np.inf)
+    for intra in (0, 1):
+        st = gpu.BasisStore(ctx, panels * w)
+        o_done, o_msg, o_led = oracle_run(v, intra)
+        noisy = oracle_run(vp, intra)[:2] != (o_done, o_msg)
+        g_done, g_msg = 0, ""
+        for p in range(panels):
+            try:
+                gpu.bcgs2(st, ctx.from_host(v[:, p * w:(p + 1) * w]), intra, th if intra else None)
+            except gpu.Error as e:
+                g_msg = str(e)
+                break
+            g_done += 1
+        if intra == 1:
+            assert o_done == g_done == panels, (o_msg, g_msg)
+            assert orth_err(st.basis_copy()) < 1e-13
+        elif noisy:
+            # the reference itself may complete or break down here (its pivot
+            # sits at the floor): the GPU must do one of the two cleanly
+            assert g_msg == "" or g_msg.split(" at step")[0] == "cholqr: nonpositive Cholesky pivot", g_msg
+        else:
+            assert g_done == o_done, (kappa, w, o_msg, g_msg)
+            assert g_msg.split(" at step")[0] == o_msg.split(" at step")[0]
+            if g_msg:
+                assert abs(int(g_msg.rsplit(" ", 1)[1]) - int(o_msg.rsplit(" ", 1)[1])) <= 2
+        if g_done == panels:
+            assert orth_err(st.basis_copy()) < 1e-13
+        if not noisy or intra == 1:
+            assert st.ledger().counts == o_led
+        st.close()
+
+
+@pytest.mark.parametrize("s", [5, 6, 10, 12, 15])
+@pytest.mark.parametrize("scheme", ["bcgs2_cholqr2", "bcgs2_randcholqr"])
+def test_c4_gmres_s_sweep(gpu, mk, orc, s, scheme):
+    """Config 4 solver leg: 2D Laplace 100^2, m = 60, s = 5..15.  Identical
+    convergence / breakdown, detail string, restart and iteration counts and
+    ledger as the reference; relres inside the config-1 envelope."""
+    from test_gpu_ops import C1_ENVELOPE
+    # 10x the reference's own one-ulp sensitivity at this s (the monomial
+    # basis condition grows with s; scripts/c1_envelope.py 6 10 12 15)
+    env = {5: C1_ENVELOPE,
+           6: [1e-10, 5e-10, 8.1e-10, 1.2e-09, 2e-09, 2.8e-09, 6.9e-07, 4e-05, 0.0081, 0.015],
+           10: [2.5e-09, 9e-08, 2e-07, 3e-07, 4e-07, 5.1e-06, 0.0047, 0.0081, 0.013, 0.017],
+           12: [9.7e-08, 3.9e-06, 9e-06, 1.5e-05, 2.6e-05, 0.00093, 0.0058, 0.013, 0.015, 0.017],
+           15: [6.3e-06, 0.00024, 0.00055, 0.00063, 0.00058, 0.0011, 0.0018, 0.0031, 0.004, 0.0049]}[s]
+    csr = orc.laplace(100, 2)
+    n = 10000
+    ctx = mk(n)
+    op = gpu.Operator.laplace(ctx, 2, 100)
+    x, rep = gpu.sstep_gmres_solve(op, ctx.from_host(np.ones(n)), ctx.from_host(np.zeros(n)), m=60, s=s, shat=60,
+                                   scheme=scheme, diagnostics=False)
+    want = orc.sstep_gmres(csr, np.ones(n), np.zeros(n), m=60, s=s, shat=60,
+                           scheme=0 if scheme == "bcgs2_cholqr2" else 1, diagnostics=False)
+    assert rep["converged"] == want.converged and rep["breakdown"] == want.breakdown
+    assert rep["breakdown_detail"] == want.breakdown_detail
+    assert (rep["restarts"], rep["iterations"]) == (want.restarts, want.iterations)
+    assert rep["reduce"] == want.reduce
+    for i, (g, w) in enumerate(zip(rep["restart_relres"], want.relres)):
+        assert abs(g - w) <= env[min(i, len(env) - 1)] * abs(w), (i, g, w)
