@@ -251,7 +251,7 @@ int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st) {
       const size_t fixed = (xt ? 2 * (size_t)nt * 8 * S * 8 * nsub : 0) + (3 * 256 + 48 + (rft ? 3 * 256 : 0)) * 8 +
                            (ki.sk == SK_COUNT ? (size_t)mh * r.K * 8 : 0) + 2 * kMaxStages * 8;
       const size_t need_red = (size_t)consumer_warps(ki.upd) * dm_len * 8;
-      const size_t need_fin = (512 + (size_t)std::max(mh, 1) * 16 + 64) * 8;
+      const size_t need_fin = (1536 + (size_t)std::max(mh, 32) * 16 + 64) * 8;  // finalize_dev scratch
       if (avail <= fixed) continue;
       int ns = (int)std::min<size_t>(kMaxStages, (avail - fixed) / stage);
       if (rowg) ns = ns / consumer_warps(false) * consumer_warps(false);  // one private sub-ring per warp
@@ -318,7 +318,8 @@ int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st) {
   if (f.ldcq == 0) f.ldcq = LDC;
   if (f.ldc == 0) f.ldc = LDC;
   a.fin = f;
-  a.fused_finalize = (ctx->world == 1) ? 1 : 0;
+  static const bool unfuse = getenv("BO_UNFUSE_FIN") != nullptr;  // diagnostics: finalize as its own kernel
+  a.fused_finalize = (ctx->world == 1 && !unfuse) ? 1 : 0;
 
   PassFn fn = get_pass_fn(nt, T, r.kind, r.exact, r.K);
   static std::mutex mu;
@@ -360,9 +361,10 @@ int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st) {
     const uint64_t bytes = rows * (8ull * ncols + (ki.sk == SK_COUNT ? 4ull : 0ull) + (ki.store ? 8ull * r.K : 0ull));
     ctx->prof.push_back({r.kind, r.K, r.p, mh, rows, bytes, pe0, pe1});
   }
-  if (ctx->world > 1) {
+  if (!a.fused_finalize) {
     // one all-reduce per pass that reduces (a ledger event); store-only passes have none
-    if (ki.qtx || ki.gram || ki.sk != SK_NONE) TRY(comm_allreduce(ctx, ctx->sums, (size_t)a.part_len, st));
+    if (ctx->world > 1 && (ki.qtx || ki.gram || ki.sk != SK_NONE))
+      TRY(comm_allreduce(ctx, ctx->sums, (size_t)a.part_len, st));
     if (f.ops) {
       finalize_kernel<<<1, 256, 0, ctx->stream>>>(f);
       CU(cudaGetLastError());

@@ -39,16 +39,25 @@ namespace bo {
 // ---------------------------------------------------------------------------
 // finalize (one CTA): the tiny factorizations after a reduction
 // ---------------------------------------------------------------------------
-static __device__ void finalize_dev(const FinArgs& f, double* smem_scratch /* >= 16*16*2 + 256*32 */) {
+static __device__ void finalize_dev(const FinArgs& f, double* smem_scratch /* >= 7*256 + 32*16 doubles */) {
+  // Every factor lives in shared memory while it is computed; global memory is
+  // read once at the start (sums, input factors, coefficient blocks) and
+  // written once at the end.
   const int tid = threadIdx.x, nth = blockDim.x;
   __shared__ int s_code;
+  __shared__ int s_fail;
+  __shared__ double s_piv;
   if (tid == 0) s_code = f.status->code;
   __syncthreads();
   if (s_code != ST_OK) return;
   const double* sums = f.sums;
   double* G = smem_scratch;             // 16 x 16
-  double* sb = smem_scratch + 256;      // 16 x 16 scratch
-  double* A = smem_scratch + 512;       // sketch block for Householder
+  double* sb = smem_scratch + 256;      // 16 x 16 scratch (Householder tau)
+  double* Rc = smem_scratch + 512;      // Cholesky factor 16 x 16
+  double* Rn = smem_scratch + 768;      // Rin 16 x 16
+  double* Rh = smem_scratch + 1024;     // Householder R 16 x 16
+  double* Rk = smem_scratch + 1280;     // Rcheck diagonal
+  double* A = smem_scratch + 1536;      // sketch block for Householder (<= 32 x 16)
   const int K = f.K;
 
   if (f.ops & (FIN_COPY_Q | FIN_PIP)) {
@@ -61,6 +70,10 @@ static __device__ void finalize_dev(const FinArgs& f, double* smem_scratch /* >=
   if (f.ops & FIN_COPY_G) {
     for (int e = tid; e < 256; e += nth) f.Gout[e] = sums[f.off_g + e];
   }
+  if (f.ops & (FIN_COEFF | FIN_MULT))
+    for (int e = tid; e < 256; e += nth) Rn[e] = f.Rin[e];
+  if (f.ops & FIN_CHECK_DIAG)
+    for (int e = tid; e < 16; e += nth) Rk[e] = f.Rcheck[e + e * kRld];
   if (f.ops & (FIN_HH | FIN_COPY_S)) {
     // S = sketch block (mh x K); count-gauss: S = Theta_g^T * count (sequential sums,
     // proj/src/dense.cpp:28-42 order)
@@ -81,35 +94,39 @@ static __device__ void finalize_dev(const FinArgs& f, double* smem_scratch /* >=
     }
     __syncthreads();
     if (f.ops & FIN_HH) {
-      tiny::householder_r(A, mh, mh, K, f.Rhh, sb);
+      tiny::householder_r(A, mh, mh, K, Rh, sb);
       __syncthreads();
+      for (int e = tid; e < 256; e += nth) f.Rhh[e] = Rh[e];
       if (tid == 0) {
         for (int j = 0; j < K; ++j)
-          if (f.Rhh[j + j * kRld] == 0.0) {  // apply_inv_upper throws SingularTriangular(j)
+          if (Rh[j + j * kRld] == 0.0) {  // apply_inv_upper throws SingularTriangular(j)
             f.status->code = ST_SINGULAR;
             f.status->pass = f.pass_id;
             f.status->step = j;
             f.status->pivot = 0.0;
+            s_code = ST_SINGULAR;
             break;
           }
       }
       __syncthreads();
-      if (f.status->code != ST_OK) return;
+      if (s_code != ST_OK) return;
     }
   }
   if (f.ops & FIN_CHECK_DIAG) {
+    __syncthreads();
     if (tid == 0) {
       for (int j = 0; j < K; ++j)
-        if (f.Rcheck[j + j * kRld] == 0.0) {
+        if (Rk[j] == 0.0) {
           f.status->code = ST_SINGULAR;
           f.status->pass = f.pass_id;
           f.status->step = j;
           f.status->pivot = 0.0;
+          s_code = ST_SINGULAR;
           break;
         }
     }
     __syncthreads();
-    if (f.status->code != ST_OK) return;
+    if (s_code != ST_OK) return;
   }
   if (f.ops & FIN_CHOL) {
     // G = GRAM block (optionally minus proj^T proj for BCGS-PIP, block_orth.cpp:245-251;
@@ -125,9 +142,9 @@ static __device__ void finalize_dev(const FinArgs& f, double* smem_scratch /* >=
       G[e] = g;
     }
     __syncthreads();
-    __shared__ int s_fail;
-    __shared__ double s_piv;
-    tiny::cholesky(G, K, f.pivot_tol, f.Rchol, sb, &s_fail, &s_piv);
+    tiny::cholesky(G, K, f.pivot_tol, Rc, sb, &s_fail, &s_piv);
+    __syncthreads();
+    for (int e = tid; e < 256; e += nth) f.Rchol[e] = Rc[e];
     if (s_fail) {
       if (tid == 0) {
         f.status->code = ST_CHOLESKY;
@@ -138,18 +155,21 @@ static __device__ void finalize_dev(const FinArgs& f, double* smem_scratch /* >=
       __syncthreads();
       return;
     }
+  } else if (f.ops & (FIN_COEFF | FIN_MULT)) {
+    for (int e = tid; e < 256; e += nth) Rc[e] = f.Rchol[e];
+    __syncthreads();
   }
   if (f.ops & FIN_COEFF) {
-    tiny::update_projection(f.C1, f.C2, f.ldc, f.p_total, K, f.Rin, f.coeffs);
+    tiny::update_projection(f.C1, f.C2, f.ldc, f.p_total, K, Rn, f.coeffs);
   }
   if (f.ops & (FIN_COEFF | FIN_MULT)) {
-    tiny::multiply_upper(f.Rchol, f.Rin, K, f.rjj);
+    tiny::multiply_upper(Rc, Rn, K, f.rjj);
   }
   __syncthreads();
 }
 
 static __global__ void __launch_bounds__(256) finalize_kernel(FinArgs f) {
-  __shared__ double scratch[512 + 4096];
+  __shared__ double scratch[1536 + 32 * 16];
   finalize_dev(f, scratch);
 }
 
@@ -449,7 +469,7 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
 #pragma unroll
         for (int nj = 0; nj < NT; ++nj) {
           const int r = ks * 4 + t4, c = nj * 8 + g;
-          cfr[ks][nj] = (r < p && c < K) ? -a.Cm[r + c * a.ldc] : 0.0;
+          cfr[ks][nj] = (r < p && c < K) ? -__ldg(a.Cm + r + c * a.ldc) : 0.0;  // L1: one miss per line per SM
         }
     }
     double accq[QTX ? MQT : 1][NT][2];
@@ -574,7 +594,9 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
         const uint32_t* stC = reinterpret_cast<const uint32_t*>(st + L.offC);
         double* xt = xtile + b * NSUB * KP * S;
 
-        if (!SPLIT && STORE && gtid < K) ptx::bulk_wait_read0();  // previous tile's store drained
+        // X buffer b was last stored from by tile it - 2: only the group before
+        // the most recent one (tile it - 1, other buffer) has to be drained
+        if (!SPLIT && STORE && gtid < K) ptx::bulk_wait_read1();
         ptx::mbar_wait(&full[s], (it / NS) & 1);
         if (SPLIT) ptx::named_bar_sync(2 + b, NW * 32);  // solved rows of this tile are in xt
 
