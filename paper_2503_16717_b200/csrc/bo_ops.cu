@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -105,7 +106,7 @@ __global__ void __launch_bounds__(256) spmv_stencil_kernel(int dims, IDX k, IDX 
 // in as 16-byte vector loads, so each thread keeps ~12 loads in flight instead
 // of 7 dependent-address ones per row.  Every row's sum is still formed in the
 // reference order with unfused mul/add (bit-identical to spmv_stencil_kernel).
-__global__ void __launch_bounds__(256) spmv_stencil4_kernel(int dims, uint32_t k, uint32_t row_begin, uint32_t ngroups,
+__global__ void __launch_bounds__(256, 4) spmv_stencil4_kernel(int dims, uint32_t k, uint32_t row_begin, uint32_t ngroups,
                                                             uint32_t halo_lo, const Stencil st,
                                                             const double* __restrict__ xext,
                                                             double* __restrict__ y) {
@@ -708,7 +709,13 @@ int op_apply(bo_op op, const double* x, double* y, bo_status* st) {
     if (ctx->n_global + 2 * op->k * op->k < (1ull << 31) && op->k % 4 == 0 && ctx->row_begin % 4 == 0 &&
         nl % 4 == 0 && op->halo_lo % 2 == 0 && ((uintptr_t)xe % 16) == 0 && ((uintptr_t)y % 16) == 0) {
       const uint32_t ng = (uint32_t)(nl / 4);
-      const int g4 = (int)std::max<long long>(1, std::min<long long>((long long)ctx->num_sms * 8, (ng + 255) / 256));
+      // one 4-row group per thread, no grid-stride loop: as many loads in
+      // flight as the SMs hold (ncu: the capped grid was latency-bound)
+      static const int cap = [] {
+        const char* e = getenv("BO_SPMV_CTAS");
+        return e ? atoi(e) : 1 << 30;
+      }();
+      const int g4 = (int)std::max<long long>(1, std::min<long long>((long long)cap, (ng + 255) / 256));
       spmv_stencil4_kernel<<<g4, 256, 0, ctx->stream>>>(op->dims, (uint32_t)op->k, (uint32_t)ctx->row_begin, ng,
                                                         (uint32_t)op->halo_lo, stc, xe, y);
     } else if (ctx->n_global + 2 * op->k * op->k < (1ull << 31)) {
