@@ -334,45 +334,36 @@ __global__ void __launch_bounds__(128) wide_update_trsm_kernel(const WideUpd a) 
 // ===========================================================================
 namespace {
 
-// L^T X (ml x kx) -> host (column-major ml x kx); allreduced across ranks
+// L^T X (ml x kx) -> host (column-major ml x kx); allreduced across ranks.
+// Runs on the streaming pass engine: one QTX pass (Q = L, <= 64 columns) per
+// 16-column chunk of X, so every operand streams through TMA at HBM speed
+// (the round-1 dedicated kernel loaded its tiles synchronously: ~20x slower).
 int wide_contract(bo_ctx ctx, const double* L, uint64_t ldl, int ml, const double* X, uint64_t ldx, int kx,
                   hd::Mat& out, bo_status* st) {
   if (ml > 64 || kx > 64) return set_st(st, BO_INVALID, 0, 0.0, "wide block of more than 64 columns");
-  const bool sym = (L == X && ml == kx && ldl == ldx);
-  const long long ntr = ((long long)ctx->n_local + 63) / 64;
-  const int grid = (int)std::max<long long>(1, std::min<long long>(ctx->num_sms, ntr));
-  const size_t need = (size_t)grid * 4096;
-  if (need > ctx->partials_cap) {
-    if (ctx->partials) cudaFree(ctx->partials);
-    ctx->partials_cap = need * 2;
-    CU(cudaMalloc(&ctx->partials, ctx->partials_cap * 8));
-  }
-  if (4096 > ctx->sums_cap) {
-    if (ctx->sums) cudaFree(ctx->sums);
-    ctx->sums_cap = 8192;
-    CU(cudaMalloc(&ctx->sums, ctx->sums_cap * 8));
-  }
-  WideArgs a{(long long)ctx->n_local, L, (long long)ldl, ml, X, (long long)ldx, kx, sym ? 1 : 0,
-             ctx->partials, ctx->sums, ctx->counter, ctx->status};
-  const size_t smem = (size_t)2 * 64 * 68 * 8;
-  static bool attr = false;
-  if (!attr) {
-    CU(cudaFuncSetAttribute((const void*)wide_contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
-  wide_contract_kernel<<<grid, 256, smem, ctx->stream>>>(a);
-  CU(cudaGetLastError());
-  ctx->launches++;
-  if (ctx->world > 1) {
-    TRY(comm_allreduce(ctx, ctx->sums, 4096, st));
-  }
-  std::vector<double> h(4096);
-  CU(cudaMemcpyAsync(h.data(), ctx->sums, 4096 * 8, cudaMemcpyDeviceToHost, ctx->stream));
-  CU(cudaMemcpyAsync(ctx->status_host, ctx->status, sizeof(DevStatus), cudaMemcpyDeviceToHost, ctx->stream));
-  CU(cudaStreamSynchronize(ctx->stream));
   out = hd::Mat(ml, kx);
-  for (int j = 0; j < kx; ++j)
-    for (int i = 0; i < ml; ++i) out(i, j) = h[i + j * 64];
+  const int ldq = (int)round_up((uint64_t)std::max(ml, 1), 8);
+  std::vector<double> h((size_t)ldq * 16);
+  for (int c0 = 0; c0 < kx; c0 += kMaxK) {
+    const int kc = std::min(kMaxK, kx - c0);
+    TRY(reset_status(ctx, st));
+    PassReq r{};
+    r.kind = PK_QTX;
+    r.K = kc;
+    r.V = X + (size_t)c0 * ldx;
+    r.ldv = ldx;
+    r.Q = L;
+    r.ldq = ldl;
+    r.p = ml;
+    r.pass_id = 1;
+    r.fin.ops = 0;
+    TRY(run_pass(ctx, r, st));
+    CU(cudaMemcpyAsync(h.data(), ctx->sums, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(ctx->status_host, ctx->status, sizeof(DevStatus), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    for (int j = 0; j < kc; ++j)
+      for (int i = 0; i < ml; ++i) out(i, c0 + j) = h[i + (size_t)j * ldq];
+  }
   return BO_OK;
 }
 
