@@ -178,155 +178,6 @@ __global__ void __launch_bounds__(256, 4) spmv_stencil4_kernel(int dims, uint32_
   }
 }
 
-// ===========================================================================
-// wide (<= 64 column) contraction and solve kernels for the two-stage big panel
-// ===========================================================================
-struct WideArgs {
-  long long nrows;
-  const double* L;
-  long long ldl;
-  int ml;
-  const double* X;
-  long long ldx;
-  int kx;
-  int sym;  // L == X: only upper tiles
-  double* partials;  // [grid][64*64]
-  double* sums;      // [64*64]
-  unsigned* counter;
-  DevStatus* status;
-};
-
-// out(ml x kx) = L^T X ; CTA walks 64-row tiles, each warp owns fixed 8x8
-// output tiles (DMMA), last CTA sums the CTA partials in fixed order.
-__global__ void __launch_bounds__(256) wide_contract_kernel(const WideArgs a) {
-  constexpr int TR = 64, S = TR + 4;
-  extern __shared__ __align__(16) double wsm[];
-  double* Ls = wsm;                // [ml][S]
-  double* Xs = wsm + 64 * S;       // [kx][S]
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
-  if (a.status->code != ST_OK) return;
-  const int mt = (a.ml + 7) / 8, nt = (a.kx + 7) / 8;
-  int tiles[8][2];
-  int ntile = 0;
-  // valid 8x8 output tiles in row-major order; warp w owns every 8th one
-  for (int idx = 0, cnt = 0; idx < 64; ++idx) {
-    const int mi = idx / 8, nj = idx % 8;
-    if (mi >= mt || nj >= nt || (a.sym && mi > nj)) continue;
-    if (cnt % 8 == warp && ntile < 8) {
-      tiles[ntile][0] = mi;
-      tiles[ntile][1] = nj;
-      ++ntile;
-    }
-    ++cnt;
-  }
-  double acc[8][2];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) acc[q][0] = acc[q][1] = 0.0;
-  const long long ntiles_rows = (a.nrows + TR - 1) / TR;
-  for (long long tr = blockIdx.x; tr < ntiles_rows; tr += gridDim.x) {
-    const long long row0 = tr * TR;
-    __syncthreads();
-    for (int e = tid; e < a.ml * TR; e += blockDim.x) {
-      const int c = e / TR, r = e % TR;
-      Ls[c * S + r] = (row0 + r < a.nrows) ? a.L[c * a.ldl + row0 + r] : 0.0;
-    }
-    if (!a.sym)
-      for (int e = tid; e < a.kx * TR; e += blockDim.x) {
-        const int c = e / TR, r = e % TR;
-        Xs[c * S + r] = (row0 + r < a.nrows) ? a.X[c * a.ldx + row0 + r] : 0.0;
-      }
-    __syncthreads();
-    const double* Xp = a.sym ? Ls : Xs;
-    for (int ks = 0; ks < TR / 4; ++ks) {
-      const int r = ks * 4 + t4;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        if (q < ntile) {
-          const int ca = tiles[q][0] * 8 + g, cb = tiles[q][1] * 8 + g;
-          const double av = ca < a.ml ? Ls[ca * S + r] : 0.0;
-          const double bv = cb < a.kx ? Xp[cb * S + r] : 0.0;
-          ptx::dmma(acc[q][0], acc[q][1], av, bv);
-        }
-      }
-    }
-  }
-  // CTA partial: every output entry is owned by exactly one warp
-  double* part = a.partials + (size_t)blockIdx.x * 4096;
-  __syncthreads();
-  for (int e = tid; e < 4096; e += blockDim.x) part[e] = 0.0;
-  __syncthreads();
-#pragma unroll
-  for (int q = 0; q < 8; ++q)
-    if (q < ntile) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int i = tiles[q][0] * 8 + g, j = tiles[q][1] * 8 + 2 * t4 + e;
-        part[i + j * 64] = acc[q][e];
-        if (a.sym && tiles[q][0] < tiles[q][1]) part[j + i * 64] = acc[q][e];
-      }
-    }
-  cta_tree_reduce(a.partials, 4096, a.sums, a.counter);
-}
-
-struct WideUpd {
-  long long nrows;
-  const double* V;
-  long long ldv;
-  int kx;
-  const double* Q;  // optional update  X = V - Q C
-  long long ldq;
-  int p;
-  const double* C;  // p x kx, ld 64
-  const double* R;  // optional solve X R^{-1}, kx x kx, ld 64
-  double* out;
-  long long ldo;
-  DevStatus* status;
-};
-
-// thread per row: X = (V - Q C) R^{-1}, right-looking substitution
-__global__ void __launch_bounds__(128) wide_update_trsm_kernel(const WideUpd a) {
-  extern __shared__ __align__(16) double wus[];
-  double* Cs = wus;              // [64 * 64]
-  double* Rs = wus + 64 * 64;    // [64 * 64]
-  double* rinv = wus + 2 * 64 * 64;
-  if (a.status->code != ST_OK) return;
-  for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) {
-    Cs[e] = a.Q ? a.C[e] : 0.0;
-    Rs[e] = a.R ? a.R[e] : 0.0;
-  }
-  __syncthreads();
-  if (threadIdx.x < 64) rinv[threadIdx.x] = a.R ? 1.0 / Rs[threadIdx.x * 65] : 1.0;
-  __syncthreads();
-  const int kx = a.kx;
-  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < a.nrows; r += (long long)gridDim.x * blockDim.x) {
-    double x[64];
-#pragma unroll
-    for (int j = 0; j < 64; ++j) x[j] = j < kx ? a.V[j * a.ldv + r] : 0.0;
-    if (a.Q) {
-      for (int i = 0; i < a.p; ++i) {
-        const double q = a.Q[i * a.ldq + r];
-#pragma unroll
-        for (int j = 0; j < 64; ++j)
-          if (j < kx) x[j] = fma(-q, Cs[i + j * 64], x[j]);
-      }
-    }
-    if (a.R) {
-#pragma unroll
-      for (int j = 0; j < 64; ++j) {
-        if (j < kx) {
-          x[j] *= rinv[j];
-#pragma unroll
-          for (int l = j + 1; l < 64; ++l)
-            if (l < kx) x[l] = fma(-Rs[j + l * 64], x[j], x[l]);
-        }
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 64; ++j)
-      if (j < kx) a.out[j * a.ldo + r] = x[j];
-  }
-}
-
 }  // namespace bo
 
 // ===========================================================================
@@ -367,35 +218,82 @@ int wide_contract(bo_ctx ctx, const double* L, uint64_t ldl, int ml, const doubl
   return BO_OK;
 }
 
-// out = (V - Q C) R^{-1} (either part optional), kx <= 64 columns
+// out = (V - Q C) R^{-1} (either part optional), kx <= 64 columns, on the
+// streaming pass engine in 16-column blocks:
+//   update      out_b = V_b - Q C_b                               (UPD_ST)
+//   solve       out_b = (out_b - out_{<b} R_{<b,b}) R_bb^{-1}     (P1_ST / UPD_POST_ST)
+// (blocked forward substitution; block b reads the solved blocks before it).
+// out may alias V.  The round-1 thread-per-row kernel was instruction-bound
+// (one shared load per FMA, 64-wide registers): ~10x slower.
 int wide_update_trsm(bo_ctx ctx, const double* V, uint64_t ldv, int kx, const double* Q, uint64_t ldq, int p,
                      const hd::Mat* C, const hd::Mat* R, double* out, uint64_t ldo, bo_status* st) {
-  std::vector<double> hc(4096, 0.0), hr(4096, 0.0);
-  if (C)
-    for (size_t j = 0; j < C->c; ++j)
-      for (size_t i = 0; i < C->r; ++i) hc[i + j * 64] = (*C)(i, j);
-  if (R)
-    for (size_t j = 0; j < R->c; ++j)
-      for (size_t i = 0; i <= j && i < R->r; ++i) hr[i + j * 64] = (*R)(i, j);
-  double* dbuf = nullptr;
-  CU(cudaMallocAsync((void**)&dbuf, 8192 * 8, ctx->stream));
-  CU(cudaMemcpyAsync(dbuf, hc.data(), 4096 * 8, cudaMemcpyHostToDevice, ctx->stream));
-  CU(cudaMemcpyAsync(dbuf + 4096, hr.data(), 4096 * 8, cudaMemcpyHostToDevice, ctx->stream));
-  WideUpd a{(long long)ctx->n_local, V, (long long)ldv, kx, (Q && p > 0) ? Q : nullptr, (long long)ldq, p,
-            dbuf, R ? dbuf + 4096 : nullptr, out, (long long)ldo, ctx->status};
-  const int grid = (int)std::max<long long>(1, std::min<long long>(ctx->num_sms * 4, ((long long)ctx->n_local + 127) / 128));
-  const size_t smem = (2 * 64 * 64 + 64) * 8;
-  static bool attr = false;
-  if (!attr) {
-    CU(cudaFuncSetAttribute((const void*)wide_update_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)smem));
-    attr = true;
+  if (kx > 64 || p > 64) return set_st(st, BO_INVALID, 0, 0.0, "wide block of more than 64 columns");
+  std::vector<double> hc((size_t)LDC * 16), hr(256);
+  const double* src = V;
+  uint64_t lds = ldv;
+  if (Q && p > 0 && C) {
+    for (int b0 = 0; b0 < kx; b0 += kMaxK) {
+      const int kb = std::min(kMaxK, kx - b0);
+      std::fill(hc.begin(), hc.end(), 0.0);
+      for (int j = 0; j < kb; ++j)
+        for (int i = 0; i < p; ++i) hc[i + (size_t)j * LDC] = (*C)(i, b0 + j);
+      CU(cudaMemcpyAsync(T_(ctx, OFF_C1), hc.data(), hc.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+      TRY(reset_status(ctx, st));
+      PassReq r{};
+      r.kind = PK_UPD_ST;
+      r.K = kb;
+      r.V = V + (size_t)b0 * ldv;
+      r.ldv = ldv;
+      r.Q = Q;
+      r.ldq = ldq;
+      r.p = p;
+      r.Cm = T_(ctx, OFF_C1);
+      r.out = out + (size_t)b0 * ldo;
+      r.ldo = ldo;
+      r.pass_id = 1;
+      TRY(run_pass(ctx, r, st));
+      CU(cudaStreamSynchronize(ctx->stream));  // hc is reused by the next block
+    }
+    src = out;
+    lds = ldo;
   }
-  wide_update_trsm_kernel<<<grid, 128, smem, ctx->stream>>>(a);
-  CU(cudaGetLastError());
-  ctx->launches++;
-  CU(cudaFreeAsync(dbuf, ctx->stream));
-  CU(cudaStreamSynchronize(ctx->stream));  // host vectors must outlive the copies
+  if (R) {
+    for (int b0 = 0; b0 < kx; b0 += kMaxK) {
+      const int kb = std::min(kMaxK, kx - b0);
+      std::fill(hr.begin(), hr.end(), 0.0);
+      for (int j = 0; j < kb; ++j)
+        for (int i = 0; i <= j; ++i) hr[i + j * 16] = (*R)(b0 + i, b0 + j);
+      std::fill(hc.begin(), hc.end(), 0.0);
+      for (int j = 0; j < kb; ++j)
+        for (int i = 0; i < b0; ++i) hc[i + (size_t)j * LDC] = (*R)(i, b0 + j);
+      CU(cudaMemcpyAsync(T_(ctx, OFF_R4), hr.data(), hr.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+      CU(cudaMemcpyAsync(T_(ctx, OFF_C1), hc.data(), hc.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+      TRY(reset_status(ctx, st));
+      PassReq r{};
+      r.K = kb;
+      r.V = src + (size_t)b0 * lds;
+      r.ldv = lds;
+      r.out = out + (size_t)b0 * ldo;
+      r.ldo = ldo;
+      r.pass_id = 1;
+      if (b0 == 0) {
+        r.kind = PK_P1_ST;
+        r.Rpre0 = T_(ctx, OFF_R4);
+      } else {
+        r.kind = PK_UPD_POST_ST;
+        r.Q = out;
+        r.ldq = ldo;
+        r.p = b0;
+        r.Cm = T_(ctx, OFF_C1);
+        r.Rpost = T_(ctx, OFF_R4);
+      }
+      TRY(run_pass(ctx, r, st));
+      CU(cudaStreamSynchronize(ctx->stream));
+    }
+  } else if (!(Q && p > 0 && C) && out != V) {
+    CU(cudaMemcpy2DAsync(out, ldo * 8, V, ldv * 8, ctx->n_local * 8, kx, cudaMemcpyDeviceToDevice, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+  }
   return BO_OK;
 }
 
