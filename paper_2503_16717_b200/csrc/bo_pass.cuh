@@ -287,6 +287,11 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
   constexpr int GT = GW * 32;
   constexpr int GBAR = SPLIT ? 6 : 1;      // named barrier of the U/S/R group
   constexpr bool XT = (NPRE > 0) || UPD || (NPOST > 0);  // X lives in the X tile
+  // Update passes without a pre-solve compute X in place in the stage's V
+  // block (each row group is owned by one warp): no X tile, so the stage ring
+  // keeps two stages at 128-row tiles even for 88-column stages (p = 55 +
+  // the 22-row sketch).  The stage is released once its bulk store has read it.
+  constexpr bool XIN = UPD && NPRE == 0;
   constexpr int KP = NT * 8;               // padded panel width
   constexpr int MQT = kMaxPTile / 8;
   constexpr int MST = 4;
@@ -317,7 +322,7 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
   const int NS = a.nstages;
   double* stages = reinterpret_cast<double*>(smem_raw);
   double* xtile = stages + a.region0_dbl;                         // [2][NSUB][KP][S]
-  double* rfac = xtile + ((XT && !ROWG) ? 2 * NSUB * KP * S : 0); // [3][256]
+  double* rfac = xtile + ((XT && !ROWG && !XIN) ? 2 * NSUB * KP * S : 0); // [3][256]
   double* rinv = rfac + 3 * 256;                                  // [3][16]
   constexpr bool RFT = KC > 0 && !EXACT && (NPRE > 0 || NPOST > 0);
   double* rft = rinv + 48;                                        // [3][256] row-major R, 1/r_jj on the diagonal
@@ -352,7 +357,7 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
       for (int e = tid; e < (mq * 8 - ncolQ) * S; e += blockDim.x) st[L.offQ + q * mq * 8 * S + ncolQ * S + e] = 0.0;
       for (int e = tid; e < (ms * 8 - ncolT) * S; e += blockDim.x) st[L.offT + q * ms * 8 * S + ncolT * S + e] = 0.0;
     }
-  if (XT && !ROWG)
+  if (XT && !ROWG && !XIN)
     for (int b = 0; b < 2 * NSUB; ++b)
       for (int e = tid; e < (KP - K) * S; e += blockDim.x) xtile[b * KP * S + K * S + e] = 0.0;
   __syncthreads();
@@ -592,11 +597,11 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
         const double* stQ = st + L.offQ;
         const double* stT = st + L.offT;
         const uint32_t* stC = reinterpret_cast<const uint32_t*>(st + L.offC);
-        double* xt = xtile + b * NSUB * KP * S;
+        double* xt = XIN ? const_cast<double*>(stV) : xtile + b * NSUB * KP * S;
 
         // X buffer b was last stored from by tile it - 2: only the group before
         // the most recent one (tile it - 1, other buffer) has to be drained
-        if (!SPLIT && STORE && gtid < K) ptx::bulk_wait_read1();
+        if (!SPLIT && !XIN && STORE && gtid < K) ptx::bulk_wait_read1();
         ptx::mbar_wait(&full[s], (it / NS) & 1);
         if (SPLIT) ptx::named_bar_sync(2 + b, NW * 32);  // solved rows of this tile are in xt
 
@@ -767,6 +772,7 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
             }
           }
         }
+        if (XIN && STORE && gtid < K) ptx::bulk_wait_read0();  // the X columns live in the stage
         release(it, s);
         if (SPLIT) {
           if (STORE && gtid < K) ptx::bulk_wait_read0();
