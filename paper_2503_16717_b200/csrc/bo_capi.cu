@@ -251,7 +251,7 @@ int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st) {
       // row-major copies of the solve factors (bo_pass.cuh RFT) in K-specialised solve passes
       const bool rft = !r.exact && (ki.npre > 0 || ki.npost > 0) && (r.K == 6 || r.K == 11 || r.K == 16);
       const size_t fixed = (xt ? 2 * (size_t)nt * 8 * S * 8 * nsub : 0) + (3 * 256 + 48 + (rft ? 3 * 256 : 0)) * 8 +
-                           (ki.sk == SK_COUNT ? (size_t)mh * r.K * 8 : 0) + 2 * kMaxStages * 8;
+                           (ki.sk == SK_COUNT ? (size_t)mh * r.K * 8 : 0) + 3 * kMaxStages * 8;
       const size_t need_red = (size_t)consumer_warps(ki.upd) * dm_len * 8;
       const size_t need_fin = (1536 + (size_t)std::max(mh, 32) * 16 + 64) * 8;  // finalize_dev scratch
       if (avail <= fixed) continue;

@@ -287,11 +287,13 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
   constexpr int GT = GW * 32;
   constexpr int GBAR = SPLIT ? 6 : 1;      // named barrier of the U/S/R group
   constexpr bool XT = (NPRE > 0) || UPD || (NPOST > 0);  // X lives in the X tile
-  // Update passes without a pre-solve compute X in place in the stage's V
-  // block (each row group is owned by one warp): no X tile, so the stage ring
-  // keeps two stages at 128-row tiles even for 88-column stages (p = 55 +
-  // the 22-row sketch).  The stage is released once its bulk store has read it.
-  constexpr bool XIN = UPD && NPRE == 0;
+  // X is computed in place in the stage's V block (each row / row group is
+  // owned by one thread / warp): no separate X tile, so the stage ring keeps
+  // two stages at 128-row tiles even for 88-column stages (p = 55 + the
+  // 22-row sketch), and the row-solve warps of pre-solve passes can run a
+  // whole ring ahead (per-stage "solved" mbarriers) instead of two tiles.
+  // A stage is released once its bulk store has read it.
+  constexpr bool XIN = (UPD && NPRE == 0) || SPLIT;  // (pre-solve passes: the row solves write X in place)
   constexpr int KP = NT * 8;               // padded panel width
   constexpr int MQT = kMaxPTile / 8;
   constexpr int MST = 4;
@@ -330,12 +332,14 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(cacc + ((SK == SK_COUNT) ? mh * K : 0));
   uint64_t* full = bars;
   uint64_t* empty = bars + kMaxStages;
+  uint64_t* solved = bars + 2 * kMaxStages;  // pre-solve passes: X of the stage is ready
   __shared__ int s_skip;
 
   if (tid == 0) {
     s_skip = a.status->code != ST_OK;
     for (int s = 0; s < NS; ++s) {
       ptx::mbar_init(&full[s], 1);
+      if (SPLIT) ptx::mbar_init(&solved[s], GAW);
       if (BO_PRODUCER_WARP) ptx::mbar_init(&empty[s], ROWG ? 1 : NW);
       else reinterpret_cast<unsigned*>(&empty[s])[0] = 0u;  // arrival counter
     }
@@ -551,9 +555,9 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
         const long long row0 = (long long)(blockIdx.x + (long long)it * gridDim.x) * T;
         const int valid = (int)(nrows - row0 < T ? nrows - row0 : T);
         const double* stV = stages + (size_t)s * L.stage + L.offV;
-        double* xt = xtile + b * NSUB * KP * S;
+        double* xt = const_cast<double*>(stV);  // X in place
+        (void)b;
         ptx::mbar_wait(&full[s], (it / NS) & 1);
-        if (it >= 2) ptx::named_bar_sync(4 + b, NW * 32);  // X buffer b drained by the U/S/R group
         {
           constexpr int GAWX = GAW ? GAW : 1;
           constexpr int RPT = (T + GAWX * 32 - 1) / (GAWX * 32);  // rows per thread
@@ -581,11 +585,10 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
             }
           }
         }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&solved[s]);  // X of tile it is in the stage
         release(it, s);
-        ptx::named_bar_arrive(2 + b, NW * 32);  // X buffer b full
       }
-      for (int it = (my_tiles >= 2 ? my_tiles - 2 : 0); it < my_tiles; ++it)
-        ptx::named_bar_sync(4 + (it & 1), NW * 32);  // consume the trailing drain signals
     } else {
       // ------------------------------------------- U / A' / S / R group
       for (int it = 0; it < my_tiles; ++it) {
@@ -603,7 +606,7 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
         // the most recent one (tile it - 1, other buffer) has to be drained
         if (!SPLIT && !XIN && STORE && gtid < K) ptx::bulk_wait_read1();
         ptx::mbar_wait(&full[s], (it / NS) & 1);
-        if (SPLIT) ptx::named_bar_sync(2 + b, NW * 32);  // solved rows of this tile are in xt
+        if (SPLIT) ptx::mbar_wait(&solved[s], (it / NS) & 1);  // solved rows of this tile are in the stage
 
         // ---- U: X = X0 - Q C on tensor cores (rows past the matrix are zero in
         // the stage and the coefficients past p / K are zero: no masks)
@@ -774,10 +777,6 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
         }
         if (XIN && STORE && gtid < K) ptx::bulk_wait_read0();  // the X columns live in the stage
         release(it, s);
-        if (SPLIT) {
-          if (STORE && gtid < K) ptx::bulk_wait_read0();
-          ptx::named_bar_arrive(4 + b, NW * 32);  // X buffer b may be refilled
-        }
       }
       if (STORE && gtid < K) ptx::bulk_wait0();
     }
