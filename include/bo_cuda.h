@@ -286,6 +286,9 @@ typedef struct {
   /* phase timings (ms, device events): sketch build, mpk, block orth, small dense
    * + x update, true residual, diagnostics */
   double t_sketch, t_mpk, t_orth, t_update, t_residual, t_diag;
+  /* device time (CUDA events on the ctx stream) from the first restart
+   * cycle's start to the last one's end: solver setup / teardown excluded */
+  double t_cycles;
 } bo_solve_report;
 
 /* sstep_gmres_solve (gmres.hpp:92, gmres.cpp:270-512): b, x0, x device shards */

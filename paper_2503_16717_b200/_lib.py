@@ -43,6 +43,7 @@ class SolveReport(C.Structure):
         ("orth", C.c_double * 256), ("arnoldi", C.c_double * 256),
         ("t_sketch", C.c_double), ("t_mpk", C.c_double), ("t_orth", C.c_double),
         ("t_update", C.c_double), ("t_residual", C.c_double), ("t_diag", C.c_double),
+        ("t_cycles", C.c_double),
     ]
 
 

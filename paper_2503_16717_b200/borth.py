@@ -795,6 +795,6 @@ def sstep_gmres_solve(op: Operator, b, x0, *, m=60, s=5, shat=60, scheme="bcgs2_
         "restart_relres": list(rep.relres)[:nh], "restart_lsq_residual": list(rep.lsq)[:nh],
         "restart_orth_error": list(rep.orth)[:nh], "restart_arnoldi_resid": list(rep.arnoldi)[:nh],
         "t_ms": {"sketch": rep.t_sketch, "mpk": rep.t_mpk, "orth": rep.t_orth, "update": rep.t_update,
-                 "residual": rep.t_residual, "diag": rep.t_diag},
+                 "residual": rep.t_residual, "diag": rep.t_diag, "cycles": rep.t_cycles},
     }
     return x, out

@@ -495,7 +495,23 @@ extern "C" int bo_sstep_gmres(bo_op op, const double* b, const double* x0, const
   } fb{store};
 
   bool done = false;
+  auto t_cycle0 = std::chrono::steady_clock::now();
+  cudaEvent_t ev_c0 = nullptr, ev_c1 = nullptr;
+  CU(cudaEventCreate(&ev_c0));
+  CU(cudaEventCreate(&ev_c1));
+  struct FreeEv {
+    cudaEvent_t a, b;
+    ~FreeEv() {
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+    }
+  } fev{ev_c0, ev_c1};
+  CU(cudaEventRecord(ev_c0, ctx->stream));
   for (uint64_t cycle = 0; cycle < cfg->max_restarts && !done; ++cycle) {
+    if (trace_on() && cycle > 0)
+      fprintf(stderr, "[bo] cycle %llu wall %.3f ms (phases so far: sketch %.3f mpk %.3f orth %.3f)\n",
+              (unsigned long long)(cycle - 1), ms_since(t_cycle0), rep->t_sketch, rep->t_mpk, rep->t_orth);
+    t_cycle0 = std::chrono::steady_clock::now();
     rep->restarts++;
     const double cycle_gamma = gamma;
     bo_basis_reset(store);
@@ -633,8 +649,12 @@ extern "C" int bo_sstep_gmres(bo_op op, const double* b, const double* x0, const
       done = true;
     }
   }
+  CU(cudaEventRecord(ev_c1, ctx->stream));
   acc_ledger(extra);
   rep->final_relres = gamma / gamma0;
   CU(cudaStreamSynchronize(ctx->stream));
+  float ms_c = 0.f;
+  CU(cudaEventElapsedTime(&ms_c, ev_c0, ev_c1));
+  rep->t_cycles = ms_c;
   return BO_OK;
 }
