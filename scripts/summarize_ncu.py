@@ -22,7 +22,8 @@ keys = {"duration_ms": "gpu__time_duration.sum", "dram_read_GB": "dram__bytes_re
         "regs": "launch__registers_per_thread", "threads": "launch__block_size",
         "smem_dyn_KB": "launch__shared_mem_per_block_dynamic"}
 units = dict(zip(hdr, rows[1]))
-scale = {"Gbyte": 1.0, "Mbyte": 1e-3, "Kbyte": 1e-6, "byte": 1e-9, "msecond": 1.0, "usecond": 1e-3, "nsecond": 1e-6}
+scale = {"Gbyte": 1.0, "Mbyte": 1e-3, "Kbyte": 1e-6, "byte": 1e-9, "msecond": 1.0, "usecond": 1e-3, "nsecond": 1e-6,
+         "ms": 1.0, "us": 1e-3, "ns": 1e-6, "GB": 1.0, "MB": 1e-3, "KB": 1e-6}
 res = {"capture": note, "note": "ncu replays are cold-cache and serialised: compare shares, not absolutes",
        "kernels": []}
 for i, r in enumerate(data):
