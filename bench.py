@@ -431,8 +431,13 @@ def main():
         side5 = round((n * world) ** (1.0 / 3.0))
         n5 = side5 ** 3
         rb5, re5 = side5 * side5 * (side5 * rank // world), side5 * side5 * (side5 * (rank + 1) // world)
+        nid5 = None
+        if world > 1:  # a fresh NCCL id per communicator
+            obj = [P.Context.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            nid5 = obj[0]
         ctx5 = ctx if world == 1 and n5 == n else P.Context(n5, device=local, rank=rank, world=world, row_begin=rb5,
-                                                            row_end=re5, nccl_id=nid)
+                                                            row_end=re5, nccl_id=nid5)
         op5 = P.Operator.convdiff(ctx5, side5, 0.3)
         b5 = ctx5.panel(1)
         b5[0, : ctx5.n_local] = 1.0
