@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=8_000_000)
+    ap.add_argument("--n", "--rows", dest="n", type=int, default=8_000_000)
     ap.add_argument("--s", type=int, default=10)
     ap.add_argument("--panels", type=int, default=6)
     ap.add_argument("--intra", default="rand_cholqr", choices=["rand_cholqr", "cholqr2"])
@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--gmres-restarts", type=int, default=3)
     ap.add_argument("--cpu-rows", type=int, default=1 << 18)
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: collectives through torch.distributed gloo (bo_ctx_create_comm), every rank on "
+                         "cuda:LOCAL_RANK %% device_count - exercises the multi-rank bench on one GPU")
     return ap.parse_args()
 
 
@@ -205,6 +208,9 @@ def make_panels(P, ctx, torch, n_global, k, panels, kappa_panel, kappa_global, s
 
 def main():
     args = parse()
+    if os.environ.get("BO_DEBUG_HANG"):
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["BO_DEBUG_HANG"]), exit=True)
     if args.impl == "reference":
         run_reference_arm(args)
         return
@@ -215,18 +221,39 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    gloo = args.comm == "gloo"
+    if gloo:
+        local = local % torch.cuda.device_count()
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if gloo:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
+
+    def allmax(x):
+        """max over ranks of a host float (CPU tensor under gloo)"""
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if gloo else torch.device("cuda", local))
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def make_ctx(nrows, r0, r1):
+        if world > 1 and gloo:
+            return P.Context(nrows, device=local, rank=rank, world=world, row_begin=r0, row_end=r1,
+                             comm=P.borth.TorchDistComm())
+        nid_ = None
+        if world > 1:  # a fresh NCCL id per communicator
+            obj = [P.Context.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            nid_ = obj[0]
+        return P.Context(nrows, device=local, rank=rank, world=world, row_begin=r0, row_end=r1, nccl_id=nid_)
+
     n = args.n
     k = args.s + 1
     rb, re_ = n * rank // world, n * (rank + 1) // world
-    nid = None
-    if world > 1:
-        obj = [P.Context.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nid = obj[0]
-    ctx = P.Context(n, device=local, rank=rank, world=world, row_begin=rb, row_end=re_, nccl_id=nid)
+    ctx = make_ctx(n, rb, re_)
     intra = P.borth.RAND_CHOLQR if args.intra == "rand_cholqr" else P.borth.CHOLQR2
     torch.cuda.set_stream(ctx.stream)  # all torch work of this script on the library stream
     panels = make_panels(P, ctx, torch, n, k, args.panels, args.kappa, args.kappa, 7)
@@ -278,9 +305,7 @@ def main():
     launches = ctx.kernel_launches - launches0
     allreduces = ctx.allreduces - ar0
     if world > 1:
-        t = torch.tensor([ms], device=ctx.device, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = allmax(ms)
         dist.barrier()
     ms_step = ms / args.steps
     value = algo_bytes / (ms_step / 1e3) / 1e9
@@ -361,9 +386,7 @@ def main():
         torch.cuda.synchronize()
         e2e_ms = (time.perf_counter() - t0) * 1e3 / nrep
         if world > 1:
-            t = torch.tensor([e2e_ms], device=ctx.device, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
+            e2e_ms = allmax(e2e_ms)
         e2e = {"value": algo_bytes / (e2e_ms / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "path": "bo_bcgs2 via ctypes; panels H2D from pinned host, basis Q and R D2H, every step; H2D / compute / D2H pipelined per panel on three streams"}
@@ -397,9 +420,7 @@ def main():
             torch.cuda.synchronize()
             ms_ = g0.elapsed_time(g1)
             if world > 1:
-                t = torch.tensor([ms_], device=ctx.device, dtype=torch.float64)
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                ms_ = float(t.item())
+                ms_ = allmax(ms_)
             return ms_, rp
 
         # per-restart time = (T(1 + R) - T(1)) / R: the solver's one-off setup
@@ -431,13 +452,7 @@ def main():
         side5 = round((n * world) ** (1.0 / 3.0))
         n5 = side5 ** 3
         rb5, re5 = side5 * side5 * (side5 * rank // world), side5 * side5 * (side5 * (rank + 1) // world)
-        nid5 = None
-        if world > 1:  # a fresh NCCL id per communicator
-            obj = [P.Context.nccl_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(obj, src=0)
-            nid5 = obj[0]
-        ctx5 = ctx if world == 1 and n5 == n else P.Context(n5, device=local, rank=rank, world=world, row_begin=rb5,
-                                                            row_end=re5, nccl_id=nid5)
+        ctx5 = ctx if world == 1 and n5 == n else make_ctx(n5, rb5, re5)
         op5 = P.Operator.convdiff(ctx5, side5, 0.3)
         b5 = ctx5.panel(1)
         b5[0, : ctx5.n_local] = 1.0
@@ -457,9 +472,7 @@ def main():
             torch.cuda.synchronize()
             ms_ = g0.elapsed_time(g1)
             if world > 1:
-                t = torch.tensor([ms_], device=ctx5.device, dtype=torch.float64)
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                ms_ = float(t.item())
+                ms_ = allmax(ms_)
             return ms_, rp
 
         m51 = timed5(1)[0]
@@ -478,7 +491,12 @@ def main():
     q = store.q_device()[: args.panels * k, : ctx.n_local]
     gq = (q @ q.T)
     if world > 1:
-        dist.all_reduce(gq)
+        if gloo:
+            gc = gq.cpu()
+            dist.all_reduce(gc)
+            gq = gc.to(gq.device)
+        else:
+            dist.all_reduce(gq)
     orth = float(torch.linalg.matrix_norm(torch.eye(gq.shape[0], device=gq.device, dtype=gq.dtype) - gq, ord=2))
 
     cpu = None

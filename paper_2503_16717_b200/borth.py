@@ -20,6 +20,7 @@ streams only; every computation is a kernel in libbo_cuda.so.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import weakref
 from dataclasses import dataclass, field
 
@@ -211,6 +212,10 @@ class TorchDistComm:
             self.dist.all_gather(parts, mine, group=self.group)
             out = self._view(recv, count * len(parts), "i8")
             out.copy_(self.torch.cat(parts).to(out.device))
+            if os.environ.get("BO_DEBUG_COMM"):
+                self.torch.cuda.synchronize()
+                print("allgather", self.dist.get_rank(), mine.tolist(), [p_.tolist() for p_ in parts],
+                      out.cpu().tolist(), flush=True)
             self.torch.cuda.synchronize()
             self.calls["allgather"] += 1
             return 0
@@ -218,27 +223,30 @@ class TorchDistComm:
             return 1
 
     def _exchange(self, user, nops, ops, stream):
+        # every rank contributes its outgoing blocks to one all-gather and
+        # picks its incoming ones (at most one block per peer and direction
+        # per group): no point-to-point matching to go wrong
         try:
             self._sync(stream)
-            reqs, recvs = [], []
+            me = self.dist.get_rank(self.group)
+            out, recvs = {}, []
             for i in range(nops):
                 o = ops[i]
                 dev = self._view(o.buf, o.count, "f8")
                 if o.is_send:
-                    h = dev.cpu()
-                    reqs.append(self.dist.isend(h, o.peer, group=self.group))
+                    out[int(o.peer)] = dev.cpu().numpy()
                 else:
-                    h = self.torch.empty(int(o.count), dtype=self.torch.float64)
-                    reqs.append(self.dist.irecv(h, o.peer, group=self.group))
-                    recvs.append((dev, h))
-            for r in reqs:
-                r.wait()
-            for dev, h in recvs:
-                dev.copy_(h)
+                    recvs.append((int(o.peer), dev))
+            allout = [None] * self.dist.get_world_size(self.group)
+            self.dist.all_gather_object(allout, out, group=self.group)
+            for peer, dev in recvs:
+                dev.copy_(self.torch.from_numpy(allout[peer][me]))
             self.torch.cuda.synchronize()
             self.calls["exchange"] += 1
             return 0
         except Exception:  # pragma: no cover
+            import traceback
+            traceback.print_exc()
             return 1
 
 

@@ -592,6 +592,9 @@ static int ctx_create_impl(int device, int rank, int world, const void* nccl_id,
     CU(cudaMalloc(&c->scratch[i], c->ld * 16 * 8));
     CU(cudaMemset(c->scratch[i], 0, c->ld * 16 * 8));
   }
+  // the initial memsets ran on the legacy stream, which the non-blocking
+  // ctx stream does not wait for
+  CU(cudaDeviceSynchronize());
   if (comm) {
     c->has_comm = true;
     c->comm = *comm;
@@ -742,8 +745,9 @@ int gen_stream(bo_ctx ctx, uint64_t mt_seed, const std::vector<std::pair<uint64_
     plan.dev = nullptr;
     const size_t words = tab.size() + (idx.size() + 3) / 4 + bo::mt64::prefix_words() + 2;
     CU(cudaMalloc((void**)&plan.dev, words * 8));
-    CU(cudaMemcpy(plan.dev, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice));
-    CU(cudaMemcpy(plan.dev + tab.size(), idx.data(), idx.size() * 2, cudaMemcpyHostToDevice));
+    CU(cudaMemcpyAsync(plan.dev, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaMemcpyAsync(plan.dev + tab.size(), idx.data(), idx.size() * 2, cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
     plan.key_total = total;
     plan.key_segs = segs;
     plan.nchunks = nc;
@@ -908,7 +912,7 @@ extern "C" int bo_sketch_from_dense(bo_ctx ctx, const double* theta, uint64_t ld
   s->ldth = ctx->ld;
   s->theta_bytes = std::max<uint64_t>(s->ldth * mhat, 1) * 8;
   CU(cudaMalloc(&s->theta, s->theta_bytes));
-  CU(cudaMemset(s->theta, 0, s->ldth * mhat * 8));
+  CU(cudaMemsetAsync(s->theta, 0, s->ldth * mhat * 8, ctx->stream));
   CU(cudaMemcpy2DAsync(s->theta, s->ldth * 8, theta, ld * 8, ctx->n_local * 8, mhat, cudaMemcpyDeviceToDevice,
                        ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
@@ -945,6 +949,7 @@ extern "C" int bo_sketch_dense_to_host(bo_sketch s, double* out, bo_status* st) 
   ok_st(st);
   if (!s->theta) return set_st(st, BO_INVALID, 0, 0.0, "sketch has no dense row stage");
   const uint64_t nl = s->ctx->n_local;
+  CU(cudaStreamSynchronize(s->ctx->stream));
   CU(cudaMemcpy2D(out, nl * 8, s->theta, s->ldth * 8, nl * 8, s->mhat, cudaMemcpyDeviceToHost));
   return BO_OK;
 }
@@ -953,7 +958,8 @@ extern "C" int bo_sketch_count_to_host(bo_sketch s, uint32_t* buckets, double* s
   if (!s->code) return set_st(st, BO_INVALID, 0, 0.0, "sketch has no count stage");
   const uint64_t nl = s->ctx->n_local;
   std::vector<uint32_t> c(nl);
-  CU(cudaMemcpy(c.data(), s->code, nl * 4, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpyAsync(c.data(), s->code, nl * 4, cudaMemcpyDeviceToHost, s->ctx->stream));
+  CU(cudaStreamSynchronize(s->ctx->stream));
   for (uint64_t i = 0; i < nl; ++i) {
     if (buckets) buckets[i] = c[i] & 0x7fffffffu;
     if (signs) signs[i] = (c[i] & 0x80000000u) ? -1.0 : 1.0;

@@ -428,7 +428,9 @@ int op_setup_halo(bo_op op, long long need_lo, long long need_hi, bo_status* st)
     uint64_t* d = nullptr;
     CU(cudaMalloc(&d, (2 + 2 * ctx->world) * 8));
     uint64_t mine[2] = {op->halo_lo, op->halo_hi};
-    CU(cudaMemcpy(d, mine, 16, cudaMemcpyHostToDevice));
+    // stream-ordered: a pageable cudaMemcpy may return before its DMA lands, and
+    // the non-blocking ctx stream does not order after the legacy stream
+    CU(cudaMemcpyAsync(d, mine, 16, cudaMemcpyHostToDevice, ctx->stream));
     TRY(comm_allgather_u64(ctx, d, 2, d + 2, st));
     std::vector<uint64_t> all(2 * ctx->world);
     CU(cudaMemcpyAsync(all.data(), d + 2, 16 * ctx->world, cudaMemcpyDeviceToHost, ctx->stream));
@@ -506,9 +508,11 @@ extern "C" int bo_op_csr(bo_ctx ctx, uint64_t ncols, const int64_t* row_ptr, con
   cudaError_t e = cudaMalloc(&op->row_ptr, (nl + 1) * 4);
   if (e == cudaSuccess) e = cudaMalloc(&op->col, std::max<uint64_t>(nnz, 1) * 4);
   if (e == cudaSuccess) e = cudaMalloc(&op->val, std::max<uint64_t>(nnz, 1) * 8);
-  if (e == cudaSuccess) e = cudaMemcpy(op->row_ptr, rp.data(), (nl + 1) * 4, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess && nnz) e = cudaMemcpy(op->col, ci.data(), nnz * 4, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess && nnz) e = cudaMemcpy(op->val, val, nnz * 8, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(op->row_ptr, rp.data(), (nl + 1) * 4, cudaMemcpyHostToDevice, ctx->stream);
+  if (e == cudaSuccess && nnz) e = cudaMemcpyAsync(op->col, ci.data(), nnz * 4, cudaMemcpyHostToDevice, ctx->stream);
+  if (e == cudaSuccess && nnz) e = cudaMemcpyAsync(op->val, val, nnz * 8, cudaMemcpyHostToDevice, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);  // rp / ci are freed on return
   if (e != cudaSuccess) {
     bo_op_destroy(op);
     return set_st(st, BO_CUDA, 0, 0.0, "CSR upload failed: %s", cudaGetErrorString(e));
