@@ -156,3 +156,21 @@ def test_sharded_gmres(gpu, tmp_path, case):
     env = C1_ENVELOPE if case == "gmres_c1" else [1e-10, 2.6e-10, 1.8e-8, 5.6e-7]
     for i, (g, w) in enumerate(zip(r["relres"], r["want_relres"])):
         assert abs(g - w) <= env[i] * abs(w), (i, g, w)
+
+
+def test_bench_world2_gloo(gpu, tmp_path):
+    """bench.py's multi-rank path (row shards, max-over-ranks timing, C3 GMRES
+    leg, e2e, orthogonality check) under torchrun with two ranks on one GPU,
+    collectives through gloo (--comm gloo)."""
+    import subprocess
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(ROOT / "bench.py"), "--gpus", "2",
+           "--comm", "gloo", "--rows", str(50 ** 3), "--steps", "3", "--warmup", "3", "--no-cpu"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=str(ROOT))
+    assert out.returncode == 0, out.stderr[-3000:]
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["orth_error"] < 1e-13
+    assert d["allreduces"] == 3 * (2 + 5 * 5)  # one physical all-reduce per ledger event
+    g = d["gmres"]
+    assert 1 <= g["restarts"] <= 4 and g["iterations"] == 60 * g["restarts"] and g["ms_per_restart"] > 0
+    assert d["e2e"]["value"] > 0
