@@ -190,6 +190,7 @@ int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st) {
   a.Cm = r.Cm;
   a.ldc = LDC;
   a.status = ctx->status;
+  a.phase_prof = ctx->phase_prof;
   int mh = 0;
   if (ki.sk == SK_GAUSS) {
     a.Th = r.sk->theta;
@@ -232,7 +233,15 @@ int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st) {
                          !ki.store && ki.npost == 0 && (r.K == 6 || r.K == 11);
   int T = 0, NS = 0;
   size_t region0 = 0, total = 0;
-  for (int want_ns : {2, 1}) {
+  // Pre-solve passes (bo_pass.cuh SPLIT) consume a tile in two hand-offs
+  // (solve warps, then the U/S/R group), so they want a deeper ring than
+  // double buffering; BO_NS_PRE sets the stage count they try for first.
+  static const int ns_pre = [] {
+    const char* e = getenv("BO_NS_PRE");
+    return e ? std::max(2, atoi(e)) : 2;
+  }();
+  const int want_hi = (ki.npre > 0 && !rowg_kind) ? ns_pre : 2;
+  for (int want_ns : {want_hi, 2, 1}) {
     for (int tt : {256, 128, 64}) {
       if (T) break;
       if (r.exact && tt != 64) continue;
@@ -622,6 +631,7 @@ extern "C" int bo_ctx_destroy(bo_ctx c) {
   cudaDeviceSynchronize();
   if (c->nccl && nccl().ok) nccl().CommDestroy(c->nccl);
   cudaFree(c->partials);
+  cudaFree(c->phase_prof);
   cudaFree(c->sums);
   cudaFree(c->counter);
   cudaFree(c->status);
@@ -1586,5 +1596,22 @@ extern "C" int bo_bcgs2(bo_basis b, const double* v, uint64_t ldv, uint64_t k, i
 extern "C" int bo_mt64_jump_window(uint64_t seed, uint64_t J, uint64_t* out312) {
   if (!bo::mt64::ready()) return BO_INVALID;
   bo::mt64::jump_window_host(seed, J, out312);
+  return BO_OK;
+}
+
+// Diagnostic: per-phase cycle counters of the pass kernels (only a library
+// built with -DBO_PHASE_PROF=1 fills them).  Copies the 16 x 16 counters to
+// out (when non-null) and zeroes them; the first call allocates them.
+extern "C" int bo_debug_phase_prof(bo_ctx ctx, unsigned long long* out) {
+  if (!ctx) return BO_INVALID;
+  if (!ctx->phase_prof) {
+    if (cudaMalloc(&ctx->phase_prof, 256 * sizeof(unsigned long long)) != cudaSuccess) return BO_CUDA;
+  } else if (out) {
+    if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return BO_CUDA;
+    if (cudaMemcpy(out, ctx->phase_prof, 256 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess)
+      return BO_CUDA;
+  }
+  if (cudaMemsetAsync(ctx->phase_prof, 0, 256 * sizeof(unsigned long long), ctx->stream) != cudaSuccess)
+    return BO_CUDA;
   return BO_OK;
 }

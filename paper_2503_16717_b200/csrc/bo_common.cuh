@@ -156,6 +156,7 @@ struct PassArgs {
   int dm_len;              // tensor-core partial length (excludes the count block)
   int fused_finalize;      // 1: last CTA runs FinArgs
   DevStatus* status;
+  unsigned long long* phase_prof;  // diagnostic builds (-DBO_PHASE_PROF=1): [16 pass shapes][16 counters]
   FinArgs fin;
 };
 

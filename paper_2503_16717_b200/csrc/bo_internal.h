@@ -11,6 +11,7 @@
 
 struct bo_ctx_s {
   int device = 0;
+  unsigned long long* phase_prof = nullptr;  // diagnostic phase counters (bo_debug_phase_prof)
   int rank = 0, world = 1;
   cudaStream_t stream = nullptr;
   bool own_stream = false;

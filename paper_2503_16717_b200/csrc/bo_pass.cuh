@@ -29,9 +29,28 @@
 #include "bo_reduce.cuh"
 
 #ifndef BO_GAW
-#define BO_GAW 2
+#define BO_GAW 2  // row-solve warps of pre-solve passes; 0: NW - 4 (see pass_kernel)
 #endif
 #include "bo_tiny.cuh"
+
+// Phase profiler (diagnostic builds only): lane 0 of every consumer warp
+// accumulates clock64() cycles per phase and adds them to
+// a.phase_prof[shape * 16 + phase] at exit (shape = NPRE * 4 + UPD * 2 + QTX).
+#ifndef BO_PHASE_PROF
+#define BO_PHASE_PROF 0
+#endif
+#if BO_PHASE_PROF
+#define PP_T0() long long pp_t = clock64()
+#define PP_MARK(i)                      \
+  do {                                  \
+    const long long pp_n = clock64();   \
+    pp_acc[i] += pp_n - pp_t;           \
+    pp_t = pp_n;                        \
+  } while (0)
+#else
+#define PP_T0() (void)0
+#define PP_MARK(i) (void)0
+#endif
 
 namespace bo {
 
@@ -282,7 +301,10 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
   constexpr int NSUB = TileGeom<T>::NSUB;  // 128-row sub-tiles per tile (T = 256: 2)
   constexpr int NW = consumer_warps(UPD);
   constexpr bool SPLIT = NPRE > 0;
-  constexpr int GAW = SPLIT ? BO_GAW : 0;  // row-solve warps (one per SM sub-partition: one row per thread)
+  // Row-solve warps.  Two, by measurement: NW - 4 (one U/S/R warp per SM
+  // sub-partition) was 3% slower over the C2 sequence, since the update is
+  // bound by the shared FP64 pipe, not by which sub-partition issues it.
+  constexpr int GAW = SPLIT ? (BO_GAW > 0 ? BO_GAW : NW - 4) : 0;
   constexpr int GW = NW - GAW;             // warps of the U/S/R group
   constexpr int GT = GW * 32;
   constexpr int GBAR = SPLIT ? 6 : 1;      // named barrier of the U/S/R group
@@ -500,11 +522,16 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
     const bool in_trsm_group = SPLIT && !ROWG && warp < GAW;
     const int gw = warp - GAW;  // warp index within the U/S/R group
     const int gtid = gw * 32 + lane;
+    // Gram accumulators of the row modes: zeroed inside each role's branch so
+    // they are not live (registers) across the row-solve warps' loop
     double gacc[NG];
-#pragma unroll
-    for (int e = 0; e < NG; ++e) gacc[e] = 0.0;
+#if BO_PHASE_PROF
+    unsigned long long pp_acc[16] = {};
+#endif
 
     if constexpr (ROWG) {
+#pragma unroll
+      for (int e = 0; e < NG; ++e) gacc[e] = 0.0;
       // ------------------------------------------- row mode (P1_GRAM)
       // warp w consumes tiles w, w + 8, ...; lane l holds rows l + 32 q
       // (q < 4): four independent rows per solve step (ILP, and one shared-
@@ -557,7 +584,9 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
         const double* stV = stages + (size_t)s * L.stage + L.offV;
         double* xt = const_cast<double*>(stV);  // X in place
         (void)b;
+        PP_T0();
         ptx::mbar_wait(&full[s], (it / NS) & 1);
+        PP_MARK(8);
         {
           constexpr int GAWX = GAW ? GAW : 1;
           constexpr int RPT = (T + GAWX * 32 - 1) / (GAWX * 32);  // rows per thread
@@ -586,11 +615,17 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
           }
         }
         __syncwarp();
+        PP_MARK(9);
         if (lane == 0) ptx::mbar_arrive(&solved[s]);  // X of tile it is in the stage
         release(it, s);
+        PP_MARK(10);
       }
+#pragma unroll
+      for (int e = 0; e < NG; ++e) gacc[e] = 0.0;
     } else {
       // ------------------------------------------- U / A' / S / R group
+#pragma unroll
+      for (int e = 0; e < NG; ++e) gacc[e] = 0.0;
       for (int it = 0; it < my_tiles; ++it) {
         const int s = it % NS, b = it & 1;
         const long long row0 = (long long)(blockIdx.x + (long long)it * gridDim.x) * T;
@@ -604,14 +639,22 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
 
         // X buffer b was last stored from by tile it - 2: only the group before
         // the most recent one (tile it - 1, other buffer) has to be drained
+        PP_T0();
         if (!SPLIT && !XIN && STORE && gtid < K) ptx::bulk_wait_read1();
         ptx::mbar_wait(&full[s], (it / NS) & 1);
+        PP_MARK(0);
         if (SPLIT) ptx::mbar_wait(&solved[s], (it / NS) & 1);  // solved rows of this tile are in the stage
+        PP_MARK(1);
 
         // ---- U: X = X0 - Q C on tensor cores (rows past the matrix are zero in
         // the stage and the coefficients past p / K are zero: no masks)
         if (UPD) {
           const double* x0 = SPLIT ? xt : stV;
+          // Each accumulator is a chain of 2 * mq dependent DMMAs; the even and
+          // odd k-steps go to separate accumulators (summed at the end) so a
+          // warp has 2 * NT independent chains in flight instead of NT.  Only
+          // in pre-solve passes: the plain update passes are HBM-bound already
+          // and the extra registers would spill their sketch accumulators.
           auto upd = [&](auto mq_c) {
             constexpr int MQc = decltype(mq_c)::value;
             for (int rg = gw; rg < T / 8; rg += GW) {
@@ -619,19 +662,25 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
               double av[2 * MQc > 0 ? 2 * MQc : 1];
 #pragma unroll
               for (int ks = 0; ks < 2 * MQc; ++ks) av[ks] = stQ[(ks * 4 + t4) * S + so(r, mq * 8)];
-              double d[NT][2];
+              double d[NT][2], d1[NT][2];
 #pragma unroll
               for (int nj = 0; nj < NT; ++nj)
 #pragma unroll
-                for (int e = 0; e < 2; ++e) d[nj][e] = x0[(nj * 8 + 2 * t4 + e) * S + so(r, KP)];
+                for (int e = 0; e < 2; ++e) {
+                  d[nj][e] = x0[(nj * 8 + 2 * t4 + e) * S + so(r, KP)];
+                  d1[nj][e] = 0.0;
+                }
 #pragma unroll
               for (int ks = 0; ks < 2 * MQc; ++ks)
 #pragma unroll
-                for (int nj = 0; nj < NT; ++nj) ptx::dmma(d[nj][0], d[nj][1], av[ks], cfr[ks][nj]);
+                for (int nj = 0; nj < NT; ++nj) {
+                  if (SPLIT && (ks & 1)) ptx::dmma(d1[nj][0], d1[nj][1], av[ks], cfr[ks][nj]);
+                  else ptx::dmma(d[nj][0], d[nj][1], av[ks], cfr[ks][nj]);
+                }
 #pragma unroll
               for (int nj = 0; nj < NT; ++nj)
 #pragma unroll
-                for (int e = 0; e < 2; ++e) xt[(nj * 8 + 2 * t4 + e) * S + so(r, KP)] = d[nj][e];
+                for (int e = 0; e < 2; ++e) xt[(nj * 8 + 2 * t4 + e) * S + so(r, KP)] = SPLIT ? d[nj][e] + d1[nj][e] : d[nj][e];
             }
           };
           switch (mq) {
@@ -645,7 +694,9 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
             case 7: upd(std::integral_constant<int, 7>{}); break;
             default: upd(std::integral_constant<int, 8>{}); break;
           }
+          PP_MARK(2);
           ptx::named_bar_sync(GBAR, GT);
+          PP_MARK(3);
         }
 
         // ---- A': post-TRSM (thread per row)
@@ -680,6 +731,7 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
           ptx::bulk_commit();
         }
 
+        PP_MARK(4);
         // ---- R: contractions on tensor cores; each warp owns k-steps
         // gw, gw + GW, ...; fragments of the next k-step are loaded before the
         // DMMAs of the current one issue
@@ -775,12 +827,29 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
             }
           }
         }
+        PP_MARK(5);
         if (XIN && STORE && gtid < K) ptx::bulk_wait_read0();  // the X columns live in the stage
+        PP_MARK(6);
         release(it, s);
+        PP_MARK(7);
       }
       if (STORE && gtid < K) ptx::bulk_wait0();
     }
 
+#if BO_PHASE_PROF
+    if (lane == 0 && a.phase_prof) {
+      constexpr int shape = NPRE * 4 + (UPD ? 2 : 0) + (QTX ? 1 : 0);
+      const bool storer = !in_trsm_group && gw == 0;  // the warp that issues the bulk stores
+      for (int i = 0; i < 11; ++i)
+        if (!(storer && i == 4)) atomicAdd(a.phase_prof + shape * 16 + i, pp_acc[i]);
+      if (storer) {
+        atomicAdd(a.phase_prof + shape * 16 + 13, pp_acc[4]);
+        atomicAdd(a.phase_prof + shape * 16 + 14, (unsigned long long)my_tiles);
+        atomicAdd(a.phase_prof + shape * 16 + 15, pp_acc[2] + pp_acc[5]);
+      }
+      atomicAdd(a.phase_prof + shape * 16 + (in_trsm_group ? 12 : 11), (unsigned long long)my_tiles);  // warp-tiles per role
+    }
+#endif
     // ---- per-warp fragments -> shared, then fixed-order sum over warps
     ptx::named_bar_sync(1, NW * 32);  // all stages consumed: reuse stage memory
     double* red = stages;             // [NW][dm_len]
