@@ -39,6 +39,9 @@
 #ifndef BO_PHASE_PROF
 #define BO_PHASE_PROF 0
 #endif
+#ifndef BO_STORE_SPREAD
+#define BO_STORE_SPREAD 1
+#endif
 #if BO_PHASE_PROF
 #define PP_T0() long long pp_t = clock64()
 #define PP_MARK(i)                      \
@@ -522,6 +525,10 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
     const bool in_trsm_group = SPLIT && !ROWG && warp < GAW;
     const int gw = warp - GAW;  // warp index within the U/S/R group
     const int gtid = gw * 32 + lane;
+    // bulk stores: column c is issued by lane c / GW of group warp c % GW, so
+    // the issue cost (proxy fence + one bulk copy per column and sub-tile) is
+    // spread over the group instead of serialising in one warp
+    const int stc = BO_STORE_SPREAD ? gw + GW * lane : gtid;
     // Gram accumulators of the row modes: zeroed inside each role's branch so
     // they are not live (registers) across the row-solve warps' loop
     double gacc[NG];
@@ -640,7 +647,7 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
         // X buffer b was last stored from by tile it - 2: only the group before
         // the most recent one (tile it - 1, other buffer) has to be drained
         PP_T0();
-        if (!SPLIT && !XIN && STORE && gtid < K) ptx::bulk_wait_read1();
+        if (!SPLIT && !XIN && STORE && stc < K) ptx::bulk_wait_read1();
         ptx::mbar_wait(&full[s], (it / NS) & 1);
         PP_MARK(0);
         if (SPLIT) ptx::mbar_wait(&solved[s], (it / NS) & 1);  // solved rows of this tile are in the stage
@@ -719,13 +726,13 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
         const double* X = XT ? xt : stV;
 
         // ---- S: bulk store of the X tile (one request per column)
-        if (STORE && gtid < K) {
+        if (STORE && stc < K) {
           ptx::fence_proxy_async_smem();
 #pragma unroll
           for (int q = 0; q < NSUB; ++q) {
             const int vq = valid - 128 * q;
             if (vq > 0)
-              ptx::bulk_s2g(a.out + (long long)gtid * a.ldo + row0 + 128 * q, xt + q * KP * S + gtid * S,
+              ptx::bulk_s2g(a.out + (long long)stc * a.ldo + row0 + 128 * q, xt + q * KP * S + stc * S,
                             (uint32_t)((((vq < 128 ? vq : 128) + 1) & ~1) * 8));
           }
           ptx::bulk_commit();
@@ -828,12 +835,12 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
           }
         }
         PP_MARK(5);
-        if (XIN && STORE && gtid < K) ptx::bulk_wait_read0();  // the X columns live in the stage
+        if (XIN && STORE && stc < K) ptx::bulk_wait_read0();  // the X columns live in the stage
         PP_MARK(6);
         release(it, s);
         PP_MARK(7);
       }
-      if (STORE && gtid < K) ptx::bulk_wait0();
+      if (STORE && stc < K) ptx::bulk_wait0();
     }
 
 #if BO_PHASE_PROF
