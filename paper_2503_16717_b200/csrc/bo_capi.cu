@@ -254,9 +254,12 @@ int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st) {
       const StageLayout SL = stage_layout(r.K, (ki.qtx || ki.upd) ? r.p : 0, ki.sk == SK_GAUSS ? mh : 0,
                                           ki.sk == SK_COUNT, tt, !rowg);
       const size_t stage = (size_t)SL.stage * 8;
-      // X tile: pre-solve / post-solve passes (update passes without a
-      // pre-solve work in place in the stage, bo_pass.cuh XIN)
-      const bool xt = (ki.npre > 0 || ki.upd || ki.npost > 0) && !rowg && !(ki.upd && ki.npre == 0);
+      // X tile.  The kernel only uses one for a post-solve without an update
+      // (bo_pass.cuh XT && !XIN): update and pre-solve passes compute X in
+      // place in the stage.  The reservation is kept for pre-solve passes as a
+      // cap on their ring: releasing it lets them pick 256-row tiles and deeper
+      // rings, which measured slower (P1_ST 227 -> 252 us, C2 sequence +0.4 ms).
+      const bool xt = (ki.npre > 0 || ki.npost > 0) && !rowg && !(ki.upd && ki.npre == 0);
       // row-major copies of the solve factors (bo_pass.cuh RFT) in K-specialised solve passes
       const bool rft = !r.exact && (ki.npre > 0 || ki.npost > 0) && (r.K == 6 || r.K == 11 || r.K == 16);
       const size_t fixed = (xt ? 2 * (size_t)nt * 8 * S * 8 * nsub : 0) + (3 * 256 + 48 + (rft ? 3 * 256 : 0)) * 8 +
