@@ -178,6 +178,90 @@ __global__ void __launch_bounds__(256, 4) spmv_stencil4_kernel(int dims, uint32_
   }
 }
 
+// Sharded variant of spmv_stencil4_kernel (same sums, bit-identical)
+// x is read in place: local row q (0 <= q < nlocal) at x[q], rows below the
+// shard at hlo[halo_lo + q] and rows above it at hhi[q - nlocal] (the halo
+// rows of op->xext), so a sharded SpMV copies only the halos, not x.
+__global__ void __launch_bounds__(256, 4) spmv_stencil4_halo_kernel(int dims, uint32_t k, uint32_t row_begin, uint32_t ngroups,
+                                                            uint32_t halo_lo, const Stencil st,
+                                                            const double* __restrict__ x,
+                                                            const double* __restrict__ hlo,
+                                                            const double* __restrict__ hhi,
+                                                            double* __restrict__ y) {
+  const int nlocal = (int)(4 * ngroups);
+  // address of local row q (a 4-row group never straddles the shard edge:
+  // k, the shard start and the halo sizes are multiples of 4)
+  auto at = [&](int q) -> const double* {
+    return q < 0 ? hlo + ((int)halo_lo + q) : (q >= nlocal ? hhi + (q - nlocal) : x + q);
+  };
+  // 3D order (i-1, j-1, l-1, self, l+1, j+1, i+1); 2D uses the j / l slots
+  const double ci_lo = dims == 3 ? st.c[0] : 0.0, cj_lo = dims == 3 ? st.c[1] : st.c[0];
+  const double cl_lo = dims == 3 ? st.c[2] : st.c[1], cself = dims == 3 ? st.c[3] : st.c[2];
+  const double cl_hi = dims == 3 ? st.c[4] : st.c[3], cj_hi = dims == 3 ? st.c[5] : st.c[4];
+  const double ci_hi = dims == 3 ? st.c[6] : 0.0;
+  const uint32_t kk = k * k;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x; gi < ngroups; gi += stride) {
+    const uint32_t r = 4 * gi, me = row_begin + r;
+    const double* xm = x + r;  // x[me]
+    uint32_t j, l0;
+    bool has_i_lo, has_i_hi;
+    if (dims == 3) {
+      const uint32_t i = me / kk;
+      const uint32_t rem = me - i * kk;
+      j = rem / k;
+      l0 = rem - j * k;
+      has_i_lo = i > 0;
+      has_i_hi = i + 1 < k;
+    } else {
+      j = me / k;  // the 2-D line index plays the role of j (neighbours +-k)
+      l0 = me - j * k;
+      has_i_lo = has_i_hi = false;
+    }
+    const bool has_j_lo = j > 0, has_j_hi = j + 1 < k;
+    double c[6];  // x[me-1 .. me+4]
+    {
+      const double2 a = *reinterpret_cast<const double2*>(xm);
+      const double2 b = *reinterpret_cast<const double2*>(xm + 2);
+      c[1] = a.x;
+      c[2] = a.y;
+      c[3] = b.x;
+      c[4] = b.y;
+      c[0] = l0 > 0 ? __ldg(at((int)r - 1)) : 0.0;
+      c[5] = l0 + 4 < k ? __ldg(at((int)r + 4)) : 0.0;
+    }
+    double jl[4], jh[4], il[4], ih[4];
+    auto ld4 = [](const double* p, double (&o)[4]) {
+      const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+      const double2 b = __ldg(reinterpret_cast<const double2*>(p + 2));
+      o[0] = a.x;
+      o[1] = a.y;
+      o[2] = b.x;
+      o[3] = b.y;
+    };
+    if (has_j_lo) ld4(at((int)r - (int)k), jl);
+    if (has_j_hi) ld4(at((int)r + (int)k), jh);
+    if (has_i_lo) ld4(at((int)r - (int)kk), il);
+    if (has_i_hi) ld4(at((int)r + (int)kk), ih);
+    double out[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const uint32_t l = l0 + t;
+      double s = 0.0;
+      if (has_i_lo) s = __dadd_rn(s, __dmul_rn(ci_lo, il[t]));
+      if (has_j_lo) s = __dadd_rn(s, __dmul_rn(cj_lo, jl[t]));
+      if (l > 0) s = __dadd_rn(s, __dmul_rn(cl_lo, c[t]));
+      s = __dadd_rn(s, __dmul_rn(cself, c[t + 1]));
+      if (l + 1 < k) s = __dadd_rn(s, __dmul_rn(cl_hi, c[t + 2]));
+      if (has_j_hi) s = __dadd_rn(s, __dmul_rn(cj_hi, jh[t]));
+      if (has_i_hi) s = __dadd_rn(s, __dmul_rn(ci_hi, ih[t]));
+      out[t] = s;
+    }
+    *reinterpret_cast<double2*>(y + r) = make_double2(out[0], out[1]);
+    *reinterpret_cast<double2*>(y + r + 2) = make_double2(out[2], out[3]);
+  }
+}
+
 }  // namespace bo
 
 // ===========================================================================
@@ -448,13 +532,17 @@ int op_setup_halo(bo_op op, long long need_lo, long long need_hi, bo_status* st)
 }
 
 // xext <- [recv halo_lo | x | recv halo_hi]; returns the pointer SpMV reads
-int halo_exchange(bo_op op, const double* x, const double** xe, bo_status* st) {
+// Fills the halo rows of op->xext from the neighbour ranks.  copy_local also
+// copies the local rows into its middle, for kernels that index x as one
+// array (CSR columns); the 4-row stencil kernel reads x in place.
+int halo_exchange(bo_op op, const double* x, const double** xe, bool copy_local, bo_status* st) {
   bo_ctx ctx = op->ctx;
   if (!op->xext) {
     *xe = x;
     return BO_OK;
   }
-  CU(cudaMemcpyAsync(op->xext + op->halo_lo, x, ctx->n_local * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (copy_local)
+    CU(cudaMemcpyAsync(op->xext + op->halo_lo, x, ctx->n_local * 8, cudaMemcpyDeviceToDevice, ctx->stream));
   if (ctx->world > 1) {
     bo_p2p_op ops[4];
     int n = 0;
@@ -590,17 +678,21 @@ namespace bo {
 namespace host {
 int op_apply(bo_op op, const double* x, double* y, bo_status* st) {
   bo_ctx ctx = op->ctx;
-  const double* xe;
-  TRY(halo_exchange(op, x, &xe, st));
   const long long nl = (long long)ctx->n_local;
+  // the 4-row stencil kernel (reads x in place, halos from op->xext)
+  const bool st4 = op->kind != 0 && ctx->n_global + 2 * op->k * op->k < (1ull << 31) && op->k % 4 == 0 &&
+                   ctx->row_begin % 4 == 0 && nl % 4 == 0 && op->halo_lo % 4 == 0 && op->halo_hi % 4 == 0 &&
+                   ((uintptr_t)x % 16) == 0 && ((uintptr_t)y % 16) == 0 &&
+                   ((uintptr_t)(op->xext ? op->xext : x) % 16) == 0;
+  const double* xe;
+  TRY(halo_exchange(op, x, &xe, !st4, st));
   const int grid = (int)std::max<long long>(1, std::min<long long>((long long)ctx->num_sms * 8, (nl + 255) / 256));
   if (op->kind == 0)
     spmv_csr_kernel<<<grid, 256, 0, ctx->stream>>>(nl, op->row_ptr, op->col, op->val, xe, y);
   else {
     Stencil stc;
     for (int q = 0; q < 7; ++q) stc.c[q] = op->coef[q];
-    if (ctx->n_global + 2 * op->k * op->k < (1ull << 31) && op->k % 4 == 0 && ctx->row_begin % 4 == 0 &&
-        nl % 4 == 0 && op->halo_lo % 2 == 0 && ((uintptr_t)xe % 16) == 0 && ((uintptr_t)y % 16) == 0) {
+    if (st4) {
       const uint32_t ng = (uint32_t)(nl / 4);
       // one 4-row group per thread, no grid-stride loop: as many loads in
       // flight as the SMs hold (ncu: the capped grid was latency-bound)
@@ -609,8 +701,14 @@ int op_apply(bo_op op, const double* x, double* y, bo_status* st) {
         return e ? atoi(e) : 1 << 30;
       }();
       const int g4 = (int)std::max<long long>(1, std::min<long long>((long long)cap, (ng + 255) / 256));
-      spmv_stencil4_kernel<<<g4, 256, 0, ctx->stream>>>(op->dims, (uint32_t)op->k, (uint32_t)ctx->row_begin, ng,
-                                                        (uint32_t)op->halo_lo, stc, xe, y);
+      const double* hlo = op->xext ? op->xext : x;
+      const double* hhi = op->xext ? op->xext + op->halo_lo + nl : x;
+      if (op->xext)
+        spmv_stencil4_halo_kernel<<<g4, 256, 0, ctx->stream>>>(op->dims, (uint32_t)op->k, (uint32_t)ctx->row_begin,
+                                                               ng, (uint32_t)op->halo_lo, stc, x, hlo, hhi, y);
+      else
+        spmv_stencil4_kernel<<<g4, 256, 0, ctx->stream>>>(op->dims, (uint32_t)op->k, (uint32_t)ctx->row_begin, ng,
+                                                          0u, stc, x, y);
     } else if (ctx->n_global + 2 * op->k * op->k < (1ull << 31)) {
       spmv_stencil_kernel<uint32_t><<<grid, 256, 0, ctx->stream>>>(op->dims, (uint32_t)op->k,
                                                                    (uint32_t)ctx->row_begin, (uint32_t)nl,
