@@ -951,6 +951,9 @@ extern "C" int bo_sketch_destroy(bo_sketch s) {
   }
   cudaFree(s->code);
   cudaFree(s->theta_g);
+  cudaFree(s->perm);
+  cudaFree(s->boff);
+  cudaFree(s->cnt);
   delete s;
   return BO_OK;
 }

@@ -72,6 +72,12 @@ struct bo_sketch_s {
   uint32_t* code = nullptr;           // count codes (local rows)
   double* theta_g = nullptr;          // count_gauss dense stage (device, mc x mhat)
   std::vector<double> theta_g_host;
+  // wide Count stages (bo_ops.cu count_apply_sorted): local rows sorted by
+  // bucket (stable: ascending row within a bucket), sign in bit 31, bucket
+  // offsets, and a device buffer for the bucket sums (mc x 16)
+  uint32_t* perm = nullptr;
+  uint32_t* boff = nullptr;
+  double* cnt = nullptr;
 };
 
 struct bo_basis_s {

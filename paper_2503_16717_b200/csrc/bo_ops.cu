@@ -7,6 +7,9 @@
 //     panel (up to 64 columns) uses the wide contraction / solve kernels here.
 #include <cuda_runtime.h>
 
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
 #include <algorithm>
 #include <cstdlib>
 #include <cmath>
@@ -262,6 +265,68 @@ __global__ void __launch_bounds__(256, 4) spmv_stencil4_halo_kernel(int dims, ui
   }
 }
 
+// ---------------------------------------------------------------------------
+// wide Count stages (thousands of buckets, e.g. count_gauss at shat = 60:
+// 7442): bucket-sorted application
+// ---------------------------------------------------------------------------
+// keys = bucket, values = local row | sign bit, and the bucket histogram
+__global__ void count_keys_kernel(const uint32_t* __restrict__ code, uint32_t n, uint32_t* __restrict__ keys,
+                                  uint32_t* __restrict__ vals, uint32_t* __restrict__ hist) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t c = code[i];
+    keys[i] = c & 0x7fffffffu;
+    vals[i] = i | (c & 0x80000000u);
+    atomicAdd(hist + (c & 0x7fffffffu), 1u);
+  }
+}
+
+// out[b + c * mc] = sum over the rows i of bucket b, ascending, of sign_i * V(i, c),
+// from +0.0 with unfused mul / add: the order of count_apply_transposed
+// (proj/src/sketch.cpp:48-62), so one GPU reproduces it bit for bit.  One
+// thread per (bucket, column); the rows' indices are prefetched eight at a
+// time so eight independent V loads are in flight per thread.
+__global__ void __launch_bounds__(256) count_apply_sorted_kernel(const uint32_t* __restrict__ perm,
+                                                                 const uint32_t* __restrict__ boff, uint32_t mc, int K,
+                                                                 const double* __restrict__ v, uint64_t ldv,
+                                                                 double* __restrict__ out) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= mc * (uint32_t)K) return;
+  const uint32_t b = t / (uint32_t)K, c = t - b * (uint32_t)K;
+  const double* vc = v + (uint64_t)c * ldv;
+  const uint32_t e = boff[b + 1];
+  double s = 0.0;
+  uint32_t q = boff[b];
+  for (; q + 8 <= e; q += 8) {
+    uint32_t pr[8];
+    double x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) pr[u] = __ldg(perm + q + u);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = __ldg(vc + (pr[u] & 0x7fffffffu));
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s = __dadd_rn(s, __dmul_rn((pr[u] & 0x80000000u) ? -1.0 : 1.0, x[u]));
+  }
+  for (; q < e; ++q) {
+    const uint32_t pr = __ldg(perm + q);
+    s = __dadd_rn(s, __dmul_rn((pr & 0x80000000u) ? -1.0 : 1.0, __ldg(vc + (pr & 0x7fffffffu))));
+  }
+  out[b + (uint64_t)c * mc] = s;
+}
+
+// S = Theta_g^T cnt (mh x K): sequential sums over the mc buckets in the
+// transpose_times order of the host stage (dense.cpp:28-42)
+__global__ void count_gauss_stage_kernel(const double* __restrict__ theta_g, const double* __restrict__ cnt,
+                                         uint32_t mc, uint32_t mh, int K, double* __restrict__ S) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= mh * (uint32_t)K) return;
+  const uint32_t i = t % mh, j = t / mh;
+  const double* a = theta_g + (uint64_t)i * mc;
+  const double* b = cnt + (uint64_t)j * mc;
+  double s = 0.0;
+  for (uint32_t r = 0; r < mc; ++r) s = __dadd_rn(s, __dmul_rn(__ldg(a + r), __ldg(b + r)));
+  S[i + (uint64_t)j * mh] = s;
+}
+
 }  // namespace bo
 
 // ===========================================================================
@@ -440,6 +505,49 @@ namespace host {
 // 64-row chunks; a Count stage with thousands of buckets is swept in bucket
 // ranges and the count_gauss dense stage is applied on the host
 // (proj/src/sketch.cpp:110-126; Theta_g is replicated).
+static bool sorted_count_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("BO_COUNT_SORTED");  // 0: the bucket-range passes (A/B, diagnostics)
+    return e ? atoi(e) != 0 : true;
+  }();
+  return on;
+}
+
+// Build the bucket-sorted row order of a Count stage once per sketch (stable
+// radix sort on the bucket, so rows stay ascending within a bucket).
+static int count_sort(bo_sketch th, bo_status* st) {
+  if (th->perm) return BO_OK;
+  bo_ctx ctx = th->ctx;
+  const uint32_t n = (uint32_t)ctx->n_local, mc = (uint32_t)th->mc;
+  uint32_t *keys = nullptr, *vals = nullptr, *keys2 = nullptr, *hist = nullptr;
+  void* tmp = nullptr;
+  size_t tb_sort = 0, tb_scan = 0;
+  int bits = 1;
+  while ((1u << bits) < mc) ++bits;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb_sort, keys, keys2, vals, th->perm, (int)n, 0, bits, ctx->stream);
+  cub::DeviceScan::ExclusiveSum(nullptr, tb_scan, hist, th->boff, (int)mc + 1, ctx->stream);
+  CU(cudaMalloc(&th->perm, std::max<size_t>(n, 1) * 4));
+  CU(cudaMalloc(&th->boff, ((size_t)mc + 1) * 4));
+  CU(cudaMalloc(&th->cnt, ((size_t)mc * 16 + (size_t)th->mhat * 16) * 8));
+  CU(cudaMalloc(&keys, std::max<size_t>(n, 1) * 4 * 3 + ((size_t)mc + 1) * 4));
+  vals = keys + std::max<uint32_t>(n, 1);
+  keys2 = vals + std::max<uint32_t>(n, 1);
+  hist = keys2 + std::max<uint32_t>(n, 1);
+  CU(cudaMalloc(&tmp, std::max(tb_sort, tb_scan)));
+  CU(cudaMemsetAsync(hist, 0, ((size_t)mc + 1) * 4, ctx->stream));
+  if (n) {
+    count_keys_kernel<<<std::max(1, std::min(ctx->num_sms * 8, (int)((n + 255) / 256))), 256, 0, ctx->stream>>>(
+        th->code, n, keys, vals, hist);
+    CU(cudaGetLastError());
+    CU(cub::DeviceRadixSort::SortPairs(tmp, tb_sort, keys, keys2, vals, th->perm, (int)n, 0, bits, ctx->stream));
+  }
+  CU(cub::DeviceScan::ExclusiveSum(tmp, tb_scan, hist, th->boff, (int)mc + 1, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  cudaFree(tmp);
+  cudaFree(keys);
+  return BO_OK;
+}
+
 int sketch_to_host(bo_sketch th, const double* v, uint64_t ldv, int K, std::vector<double>& S, bo_status* st) {
   bo_ctx ctx = th->ctx;
   const uint64_t mh = th->mhat;
@@ -463,6 +571,28 @@ int sketch_to_host(bo_sketch th, const double* v, uint64_t ldv, int K, std::vect
     return BO_OK;
   }
   const uint64_t mc = th->mc;
+  if (sorted_count_enabled() && K <= 16 && ctx->n_local < (1ull << 31)) {
+    // bucket-sorted application: one sort per sketch, then one gather pass
+    TRY(count_sort(th, st));
+    const uint32_t nt = (uint32_t)(mc * K);
+    count_apply_sorted_kernel<<<(nt + 255) / 256, 256, 0, ctx->stream>>>(th->perm, th->boff, (uint32_t)mc, K, v, ldv,
+                                                                         th->cnt);
+    CU(cudaGetLastError());
+    ctx->launches++;
+    if (ctx->world > 1) TRY(comm_allreduce(ctx, th->cnt, mc * K, st));
+    const double* res = th->cnt;
+    if (th->kind != BO_SKETCH_COUNT) {
+      const uint32_t ng = (uint32_t)(mh * K);
+      count_gauss_stage_kernel<<<(ng + 127) / 128, 128, 0, ctx->stream>>>(th->theta_g, th->cnt, (uint32_t)mc,
+                                                                           (uint32_t)mh, K, th->cnt + mc * 16);
+      CU(cudaGetLastError());
+      ctx->launches++;
+      res = th->cnt + mc * 16;
+    }
+    CU(cudaMemcpyAsync(S.data(), res, mh * K * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return BO_OK;
+  }
   const int chunk = std::max(64, 4096 / K);
   std::vector<double> cnt(mc * K, 0.0), hs;
   for (uint64_t b0 = 0; b0 < mc; b0 += chunk) {

@@ -93,6 +93,24 @@ def test_sketch_apply(gpu, mk, orc, kind):
     assert led.counts == [0, 0, 1, 0]
 
 
+@pytest.mark.parametrize("kind", ["count", "countgauss"])
+@pytest.mark.parametrize("k", [6, 11])
+def test_wide_count_apply_bitexact(gpu, mk, orc, kind, k):
+    """Count stages too wide for the fused pass (mc * k > 4096; shat = 20 gives
+    mc = 2 * 21^2 = 882 buckets) go through the bucket-sorted gather, which
+    sums each bucket in ascending row order like count_apply_transposed
+    (proj/src/sketch.cpp:48-62): bit-identical on one GPU, and so is the
+    count_gauss dense stage after it (dense.cpp:28-42 order)."""
+    n = 30011
+    v = orc.gen_glued(n, 1, k, 1e3, 1e3, 7)
+    ctx = mk(n)
+    sk = gpu.SketchOperator.build(ctx, kind, n, 20, 5)
+    out = sk.apply(ctx.from_host(v), gpu.ReduceLedger())
+    want = orc.sketch_apply(orc.sketch_build({"count": 1, "countgauss": 2}[kind], n, 20, 5).h, v)
+    assert out.shape == want.shape
+    assert np.array_equal(out, want), float(np.max(np.abs(out - want)))
+
+
 def test_ambient_too_small(gpu, mk):
     ctx = mk(22)
     with pytest.raises(gpu.AmbientTooSmall, match="ambient dimension n=22 must exceed sketch size mhat=22"):
