@@ -16,6 +16,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <future>
 #include <mutex>
 #include <random>
 #include <unordered_map>
@@ -720,6 +721,47 @@ struct HostRng {
   }
 };
 
+// The count_gauss dense stage is drawn on the host with the reference's
+// generator (bit-identical, ~15 ms for 7442 x 122).  The GMRES driver knows
+// the next restart's seed, so it asks for that stage to be drawn on a host
+// thread while the current restart runs on the GPU.
+static std::vector<double> gen_theta_g(uint64_t seed, uint64_t mc, uint64_t mhat) {
+  HostRng rg(derive_seed(seed, 1));
+  const double scale = 1.0 / std::sqrt(double(mhat));
+  std::vector<double> t(mc * mhat);
+  for (uint64_t j = 0; j < mhat; ++j)
+    for (uint64_t i = 0; i < mc; ++i) t[i + j * mc] = scale * rg.normal();
+  return t;
+}
+struct ThetaGJob {
+  uint64_t seed, mc, mhat;
+  std::future<std::vector<double>> fut;
+};
+static std::mutex g_tg_mu;
+static std::vector<ThetaGJob> g_tg_jobs;
+
+void prefetch_theta_g(uint64_t seed, uint64_t mc, uint64_t mhat) {
+  std::lock_guard<std::mutex> g(g_tg_mu);
+  for (auto& j : g_tg_jobs)
+    if (j.seed == seed && j.mc == mc && j.mhat == mhat) return;
+  if (g_tg_jobs.size() >= 2) g_tg_jobs.erase(g_tg_jobs.begin());  // (waits for a stale job to finish)
+  g_tg_jobs.push_back({seed, mc, mhat, std::async(std::launch::async, gen_theta_g, seed, mc, mhat)});
+}
+
+std::vector<double> take_theta_g(uint64_t seed, uint64_t mc, uint64_t mhat) {
+  std::future<std::vector<double>> f;
+  {
+    std::lock_guard<std::mutex> g(g_tg_mu);
+    for (size_t k = 0; k < g_tg_jobs.size(); ++k)
+      if (g_tg_jobs[k].seed == seed && g_tg_jobs[k].mc == mc && g_tg_jobs[k].mhat == mhat) {
+        f = std::move(g_tg_jobs[k].fut);
+        g_tg_jobs.erase(g_tg_jobs.begin() + k);
+        break;
+      }
+  }
+  return f.valid() ? f.get() : gen_theta_g(seed, mc, mhat);
+}
+
 struct Chunk {
   uint64_t J, len;
 };
@@ -895,11 +937,7 @@ extern "C" int bo_sketch_build(bo_ctx ctx, int kind, uint64_t n, uint64_t shat, 
   }
   if (kind == BO_SKETCH_COUNT_GAUSS) {
     // dense stage mc x mhat from derive_seed(seed, 1) (sketch.cpp:91-95), replicated
-    HostRng rg(derive_seed(seed, 1));
-    const double scale = 1.0 / std::sqrt(double(s->mhat));
-    s->theta_g_host.resize(s->mc * s->mhat);
-    for (uint64_t j = 0; j < s->mhat; ++j)
-      for (uint64_t i = 0; i < s->mc; ++i) s->theta_g_host[i + j * s->mc] = scale * rg.normal();
+    s->theta_g_host = bo::host::take_theta_g(seed, s->mc, s->mhat);
     cudaError_t e = cudaMalloc(&s->theta_g, s->theta_g_host.size() * 8);
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(s->theta_g, s->theta_g_host.data(), s->theta_g_host.size() * 8, cudaMemcpyHostToDevice,

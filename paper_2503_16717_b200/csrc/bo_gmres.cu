@@ -521,6 +521,8 @@ extern "C" int bo_sstep_gmres(bo_op op, const double* b, const double* x0, const
       TRY(bo_sketch_build(ctx, cfg->sketch, n, cfg->s, derive_seed(cfg->seed, cycle + 1), &theta, st));
     else if (cfg->scheme == BO_TWOSTAGE_RANDBCGS)
       TRY(bo_sketch_build(ctx, cfg->sketch, n, cfg->shat, derive_seed(cfg->seed, cycle + 1), &theta, st));
+    if (theta && cfg->sketch == BO_SKETCH_COUNT_GAUSS && cycle + 1 < cfg->max_restarts)  // next restart's stage
+      prefetch_theta_g(derive_seed(cfg->seed, cycle + 2), theta->mc, theta->mhat);
     struct FreeS {
       bo_sketch s;
       ~FreeS() { bo_sketch_destroy(s); }

@@ -227,6 +227,9 @@ void push_panel_host(bo_basis b, uint64_t k, const double* proj, uint64_t ldp, c
 uint64_t derive_seed(uint64_t base, uint64_t stream);
 // the context's collective transport (NCCL, or bo_comm_ops callbacks)
 int comm_allreduce(bo_ctx ctx, double* buf, size_t n, bo_status* st);
+// count_gauss dense stage for a sketch seed, drawn ahead on a host thread
+void prefetch_theta_g(uint64_t seed, uint64_t mc, uint64_t mhat);
+std::vector<double> take_theta_g(uint64_t seed, uint64_t mc, uint64_t mhat);
 int comm_allgather_u64(bo_ctx ctx, const uint64_t* send, size_t n, uint64_t* recv, bo_status* st);
 int comm_exchange(bo_ctx ctx, int nops, const bo_p2p_op* ops, bo_status* st);
 int op_apply(bo_op op, const double* x, double* y, bo_status* st);
