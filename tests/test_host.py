@@ -97,6 +97,22 @@ def test_count_rows_from_jumped_window(lib, orc):
             assert (1.0 if sg & 1 else -1.0) == so[a + t]
 
 
+@pytest.mark.parametrize("shat,seed", [(5, 11), (60, 3), (60, 987654321)])
+def test_count_gauss_dense_stage_matches_reference(lib, orc, shat, seed):
+    """The replicated count_gauss dense stage (mc x mhat; 7442 x 122 at
+    shat = 60) equals the reference's stream entry for entry
+    (sketch.cpp:91-95)."""
+    import numpy as np
+    mc, mh = 2 * (shat + 1) ** 2, 2 * (shat + 1)
+    n = max(mc, mh) + 500  # (the oracle's dense-stage accessor wants n >= mc)
+    want = orc.sketch_dense(orc.sketch_build(2, n, shat, seed).h)
+    out = np.empty(mc * mh)
+    lib.bo_debug_count_gauss_stage.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_void_p]
+    assert lib.bo_debug_count_gauss_stage(seed, mc, mh, out.ctypes.data) == 0
+    assert want.shape == (mc, mh)
+    assert np.array_equal(out.reshape((mc, mh), order="F"), want)
+
+
 # ------------------------------------------------------------ MatrixMarket --
 MM_CASES = {
     "general": "%%MatrixMarket matrix coordinate real general\n% comment\n\n3 4 5\n1 1 2.5\n3 4 -1e-3\n2 2 7\n"
