@@ -70,6 +70,13 @@ def _worker(rank, world, port, case, out_dir):
         g = P.SketchOperator.build(ctx, "gaussian", n, 5, 7).dense_stage()
         og = orc.sketch_dense(orc.sketch_build(0, n, 5, 7).h)
         res["gauss_rel"] = float(np.max(np.abs(g - og[rb:re_])) / np.max(np.abs(og)))
+        # wide Count stages (bucket-sorted gather, per-rank bucket sums + one all-reduce)
+        v = orc.gen_glued(n, 1, 6, 1e3, 1e3, 3)
+        for kind, code in (("count", 1), ("countgauss", 2)):
+            sk = P.SketchOperator.build(ctx, kind, n, 20, 5)
+            out = sk.apply(ctx.from_host(np.ascontiguousarray(v[rb:re_])), P.ReduceLedger())
+            want = orc.sketch_apply(orc.sketch_build(code, n, 20, 5).h, v)
+            res[f"wide_{kind}_rel"] = float(np.max(np.abs(out - want)) / np.max(np.abs(want)))
     elif case in ("bcgs2_rand", "bcgs2_cholqr2"):
         n, k, panels = 20_000, 11, 4
         intra = 1 if case == "bcgs2_rand" else 0
@@ -130,6 +137,7 @@ def test_sharded_sketches(gpu, tmp_path):
     r = _run("sketch", tmp_path)
     assert r["count_exact"]
     assert r["gauss_rel"] < 1e-14
+    assert r["wide_count_rel"] < 1e-13 and r["wide_countgauss_rel"] < 1e-13
 
 
 @pytest.mark.parametrize("case", ["bcgs2_rand", "bcgs2_cholqr2"])
