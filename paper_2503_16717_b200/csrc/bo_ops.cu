@@ -104,12 +104,39 @@ __global__ void __launch_bounds__(256) spmv_stencil_kernel(int dims, IDX k, IDX 
   }
 }
 
+// Four consecutive doubles (32-byte aligned) in one 256-bit access
+// (LDG.E.ENL2.256 / STG.E.ENL2.256 on sm_100): one L1 wavefront per 128-byte
+// line instead of two half-used 16-byte accesses per thread.
+#ifndef BO_SPMV_256
+#define BO_SPMV_256 1
+#endif
+__device__ __forceinline__ void double4_ld(const double* p, double& a, double& b, double& c, double& d) {
+#if BO_SPMV_256
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+#else
+  const double2 u = __ldg(reinterpret_cast<const double2*>(p));
+  const double2 v = __ldg(reinterpret_cast<const double2*>(p + 2));
+  a = u.x, b = u.y, c = v.x, d = v.y;
+#endif
+}
+__device__ __forceinline__ void double4_st(double* p, double a, double b, double c, double d) {
+#if BO_SPMV_256
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+#else
+  *reinterpret_cast<double2*>(p) = make_double2(a, b);
+  *reinterpret_cast<double2*>(p + 2) = make_double2(c, d);
+#endif
+}
+
 // Four consecutive rows per thread (same grid line when k % 4 == 0 and the
 // shard starts on a multiple of 4): the centre, +-k and +-k^2 neighbours come
 // in as 16-byte vector loads, so each thread keeps ~12 loads in flight instead
 // of 7 dependent-address ones per row.  Every row's sum is still formed in the
 // reference order with unfused mul/add (bit-identical to spmv_stencil_kernel).
-__global__ void __launch_bounds__(256, 4) spmv_stencil4_kernel(int dims, uint32_t k, uint32_t row_begin, uint32_t ngroups,
+#ifndef BO_SPMV_MINB
+#define BO_SPMV_MINB 4
+#endif
+__global__ void __launch_bounds__(256, BO_SPMV_MINB) spmv_stencil4_kernel(int dims, uint32_t k, uint32_t row_begin, uint32_t ngroups,
                                                             uint32_t halo_lo, const Stencil st,
                                                             const double* __restrict__ xext,
                                                             double* __restrict__ y) {
@@ -140,24 +167,12 @@ __global__ void __launch_bounds__(256, 4) spmv_stencil4_kernel(int dims, uint32_
     const bool has_j_lo = j > 0, has_j_hi = j + 1 < k;
     double c[6];  // x[me-1 .. me+4]
     {
-      const double2 a = *reinterpret_cast<const double2*>(xm);
-      const double2 b = *reinterpret_cast<const double2*>(xm + 2);
-      c[1] = a.x;
-      c[2] = a.y;
-      c[3] = b.x;
-      c[4] = b.y;
+      double4_ld(xm, c[1], c[2], c[3], c[4]);
       c[0] = l0 > 0 ? __ldg(xm - 1) : 0.0;
       c[5] = l0 + 4 < k ? __ldg(xm + 4) : 0.0;
     }
     double jl[4], jh[4], il[4], ih[4];
-    auto ld4 = [](const double* p, double (&o)[4]) {
-      const double2 a = __ldg(reinterpret_cast<const double2*>(p));
-      const double2 b = __ldg(reinterpret_cast<const double2*>(p + 2));
-      o[0] = a.x;
-      o[1] = a.y;
-      o[2] = b.x;
-      o[3] = b.y;
-    };
+    auto ld4 = [](const double* p, double (&o)[4]) { double4_ld(p, o[0], o[1], o[2], o[3]); };
     if (has_j_lo) ld4(xm - k, jl);
     if (has_j_hi) ld4(xm + k, jh);
     if (has_i_lo) ld4(xm - kk, il);
@@ -176,8 +191,7 @@ __global__ void __launch_bounds__(256, 4) spmv_stencil4_kernel(int dims, uint32_
       if (has_i_hi) s = __dadd_rn(s, __dmul_rn(ci_hi, ih[t]));
       out[t] = s;
     }
-    *reinterpret_cast<double2*>(y + r) = make_double2(out[0], out[1]);
-    *reinterpret_cast<double2*>(y + r + 2) = make_double2(out[2], out[3]);
+    double4_st(y + r, out[0], out[1], out[2], out[3]);
   }
 }
 
@@ -185,7 +199,7 @@ __global__ void __launch_bounds__(256, 4) spmv_stencil4_kernel(int dims, uint32_
 // x is read in place: local row q (0 <= q < nlocal) at x[q], rows below the
 // shard at hlo[halo_lo + q] and rows above it at hhi[q - nlocal] (the halo
 // rows of op->xext), so a sharded SpMV copies only the halos, not x.
-__global__ void __launch_bounds__(256, 4) spmv_stencil4_halo_kernel(int dims, uint32_t k, uint32_t row_begin, uint32_t ngroups,
+__global__ void __launch_bounds__(256, BO_SPMV_MINB) spmv_stencil4_halo_kernel(int dims, uint32_t k, uint32_t row_begin, uint32_t ngroups,
                                                             uint32_t halo_lo, const Stencil st,
                                                             const double* __restrict__ x,
                                                             const double* __restrict__ hlo,
@@ -224,24 +238,12 @@ __global__ void __launch_bounds__(256, 4) spmv_stencil4_halo_kernel(int dims, ui
     const bool has_j_lo = j > 0, has_j_hi = j + 1 < k;
     double c[6];  // x[me-1 .. me+4]
     {
-      const double2 a = *reinterpret_cast<const double2*>(xm);
-      const double2 b = *reinterpret_cast<const double2*>(xm + 2);
-      c[1] = a.x;
-      c[2] = a.y;
-      c[3] = b.x;
-      c[4] = b.y;
+      double4_ld(xm, c[1], c[2], c[3], c[4]);
       c[0] = l0 > 0 ? __ldg(at((int)r - 1)) : 0.0;
       c[5] = l0 + 4 < k ? __ldg(at((int)r + 4)) : 0.0;
     }
     double jl[4], jh[4], il[4], ih[4];
-    auto ld4 = [](const double* p, double (&o)[4]) {
-      const double2 a = __ldg(reinterpret_cast<const double2*>(p));
-      const double2 b = __ldg(reinterpret_cast<const double2*>(p + 2));
-      o[0] = a.x;
-      o[1] = a.y;
-      o[2] = b.x;
-      o[3] = b.y;
-    };
+    auto ld4 = [](const double* p, double (&o)[4]) { double4_ld(p, o[0], o[1], o[2], o[3]); };
     if (has_j_lo) ld4(at((int)r - (int)k), jl);
     if (has_j_hi) ld4(at((int)r + (int)k), jh);
     if (has_i_lo) ld4(at((int)r - (int)kk), il);
@@ -260,8 +262,7 @@ __global__ void __launch_bounds__(256, 4) spmv_stencil4_halo_kernel(int dims, ui
       if (has_i_hi) s = __dadd_rn(s, __dmul_rn(ci_hi, ih[t]));
       out[t] = s;
     }
-    *reinterpret_cast<double2*>(y + r) = make_double2(out[0], out[1]);
-    *reinterpret_cast<double2*>(y + r + 2) = make_double2(out[2], out[3]);
+    double4_st(y + r, out[0], out[1], out[2], out[3]);
   }
 }
 
@@ -812,8 +813,8 @@ int op_apply(bo_op op, const double* x, double* y, bo_status* st) {
   // the 4-row stencil kernel (reads x in place, halos from op->xext)
   const bool st4 = op->kind != 0 && ctx->n_global + 2 * op->k * op->k < (1ull << 31) && op->k % 4 == 0 &&
                    ctx->row_begin % 4 == 0 && nl % 4 == 0 && op->halo_lo % 4 == 0 && op->halo_hi % 4 == 0 &&
-                   ((uintptr_t)x % 16) == 0 && ((uintptr_t)y % 16) == 0 &&
-                   ((uintptr_t)(op->xext ? op->xext : x) % 16) == 0;
+                   ((uintptr_t)x % 32) == 0 && ((uintptr_t)y % 32) == 0 &&
+                   ((uintptr_t)(op->xext ? op->xext : x) % 32) == 0;
   const double* xe;
   TRY(halo_exchange(op, x, &xe, !st4, st));
   const int grid = (int)std::max<long long>(1, std::min<long long>((long long)ctx->num_sms * 8, (nl + 255) / 256));
