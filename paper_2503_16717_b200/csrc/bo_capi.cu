@@ -157,14 +157,17 @@ PassFn get_pass_fn(int nt, int T, int kind, bool exact, int K) {
       if (K == 6) f = pass_fn_kc6_t256(kind);
       if (K == 11) f = pass_fn_kc11_t256(kind);
       if (K == 16) f = pass_fn_kc16_t256(kind);
+      if (K == 13) f = pass_fn_kc13_t256(kind);
     } else if (T == 128) {
       if (K == 6) f = pass_fn_kc6_t128(kind);
       if (K == 11) f = pass_fn_kc11_t128(kind);
       if (K == 16) f = pass_fn_kc16_t128(kind);
+      if (K == 13) f = pass_fn_kc13_t128(kind);
     } else {
       if (K == 6) f = pass_fn_kc6_t64(kind);
       if (K == 11) f = pass_fn_kc11_t64(kind);
       if (K == 16) f = pass_fn_kc16_t64(kind);
+      if (K == 13) f = pass_fn_kc13_t64(kind);
     }
     if (f) return f;
   }
@@ -262,7 +265,7 @@ int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st) {
       // rings, which measured slower (P1_ST 227 -> 252 us, C2 sequence +0.4 ms).
       const bool xt = (ki.npre > 0 || ki.npost > 0) && !rowg && !(ki.upd && ki.npre == 0);
       // row-major copies of the solve factors (bo_pass.cuh RFT) in K-specialised solve passes
-      const bool rft = !r.exact && (ki.npre > 0 || ki.npost > 0) && (r.K == 6 || r.K == 11 || r.K == 16);
+      const bool rft = !r.exact && (ki.npre > 0 || ki.npost > 0) && (r.K == 6 || r.K == 11 || r.K == 13 || r.K == 16);
       const size_t fixed = (xt ? 2 * (size_t)nt * 8 * S * 8 * nsub : 0) + (3 * 256 + 48 + (rft ? 3 * 256 : 0)) * 8 +
                            (ki.sk == SK_COUNT ? (size_t)mh * r.K * 8 : 0) + 3 * kMaxStages * 8;
       const size_t need_red = (size_t)consumer_warps(ki.upd) * dm_len * 8;

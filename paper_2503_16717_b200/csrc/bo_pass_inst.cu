@@ -1,5 +1,5 @@
 // bo_pass_inst.cu — one instantiation unit of the streaming pass engine.
-// Compiled once per combination with -DBO_INST_NT=<1|2> or -DBO_INST_KC=<6|11|16>
+// Compiled once per combination with -DBO_INST_NT=<1|2> or -DBO_INST_KC=<6|11|13|16>
 // and -DBO_INST_T=<64|128> (or -DBO_INST_EXACT), so the build runs the heavy
 // template instantiations in parallel.
 #include "bo_internal.h"
@@ -29,7 +29,8 @@ PassFn BO_CAT(pass_fn_nt, BO_INST_NT, _t, BO_INST_T)(int kind) {
   return nullptr;
 }
 #elif defined(BO_INST_KC)
-// triangular-solve passes specialised on the panel width (s = 5, 10, 15)
+// triangular-solve passes specialised on the panel width (s = 5, 10, 12, 15; K = 13 is
+// also the last 16-column block of the two-stage big panel at shat = 60)
 PassFn BO_CAT(pass_fn_kc, BO_INST_KC, _t, BO_INST_T)(int kind) {
   constexpr int NT = BO_INST_KC <= 8 ? 1 : 2;
   switch (kind) {

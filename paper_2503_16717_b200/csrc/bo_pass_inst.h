@@ -14,6 +14,9 @@ PassFn pass_fn_nt2_t256(int kind);
 PassFn pass_fn_kc6_t256(int kind);
 PassFn pass_fn_kc11_t256(int kind);
 PassFn pass_fn_kc16_t256(int kind);
+PassFn pass_fn_kc13_t256(int kind);
+PassFn pass_fn_kc13_t128(int kind);
+PassFn pass_fn_kc13_t64(int kind);
 PassFn pass_fn_nt1_t128(int kind);
 PassFn pass_fn_nt1_t64(int kind);
 PassFn pass_fn_nt2_t128(int kind);
