@@ -100,6 +100,43 @@ __global__ void __launch_bounds__(256) xupdate_kernel(long long n, int q, const 
   }
 }
 
+// Four consecutive rows per thread with 256-bit accesses (32-byte aligned x and
+// Q columns): the same fma chain per element, in the same column order.
+__global__ void __launch_bounds__(256) xupdate4_kernel(long long ngroups, int q, const double* __restrict__ Q,
+                                                       long long ldq, const double* __restrict__ y,
+                                                       double* __restrict__ x) {
+  __shared__ double ys[256];
+  for (int j = threadIdx.x; j < q; j += blockDim.x) ys[j] = y[j];
+  __syncthreads();
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < ngroups;
+       g += (long long)gridDim.x * blockDim.x) {
+    const long long i = 4 * g;
+    double v[4];
+    asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+                 : "l"(x + i));
+    int j = 0;
+    for (; j + 8 <= q; j += 8) {
+      double c[8][4];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        asm("ld.global.cs.v4.f64 {%0, %1, %2, %3}, [%4];"
+            : "=d"(c[u][0]), "=d"(c[u][1]), "=d"(c[u][2]), "=d"(c[u][3])
+            : "l"(Q + (j + u) * ldq + i));
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] = fma(c[u][e], ys[j + u], v[e]);
+    }
+    for (; j < q; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v[e] = fma(__ldcs(Q + j * ldq + i + e), ys[j], v[e]);
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(x + i), "d"(v[0]), "d"(v[1]), "d"(v[2]),
+                 "d"(v[3])
+                 : "memory");
+  }
+}
+
 // w = aq - Q(:,0:p) h  ; partial sum of squares (Arnoldi residual column)
 __global__ void __launch_bounds__(256) arnoldi_col_kernel(long long n, int p, const double* __restrict__ Q,
                                                           long long ldq, const double* __restrict__ h,
@@ -611,8 +648,12 @@ extern "C" int bo_sstep_gmres(bo_op op, const double* b, const double* x0, const
     const double lsq = solve_lsq(H, gamma, y);
     const double t_l = ms_since(t0);
     CU(cudaMemcpyAsync(g.ydev, y.data(), q_in * 8, cudaMemcpyHostToDevice, ctx->stream));
-    xupdate_kernel<<<(unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ctx->num_sms * 8, (nl + 255) / 256)), 256, 0,
-                     ctx->stream>>>((long long)nl, (int)q_in, store->q, (long long)ld, g.ydev, x);
+    if (nl % 4 == 0 && ld % 4 == 0 && (uintptr_t)x % 32 == 0 && (uintptr_t)store->q % 32 == 0)
+      xupdate4_kernel<<<(unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ctx->num_sms * 8, (nl / 4 + 255) / 256)),
+                        256, 0, ctx->stream>>>((long long)(nl / 4), (int)q_in, store->q, (long long)ld, g.ydev, x);
+    else
+      xupdate_kernel<<<(unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ctx->num_sms * 8, (nl + 255) / 256)), 256,
+                       0, ctx->stream>>>((long long)nl, (int)q_in, store->q, (long long)ld, g.ydev, x);
     CU(cudaGetLastError());
     ctx->launches++;
     const double t_k = ms_since(t0);
