@@ -257,6 +257,14 @@ int bo_csr_host_arrays(bo_csr_host h, int64_t* row_ptr, int64_t* col, double* va
 int bo_csr_host_destroy(bo_csr_host h);
 int bo_mm_write(const char* path, uint64_t nrows, uint64_t ncols, const int64_t* row_ptr, const int64_t* col,
                 const double* val, bo_status* st);
+/* gen_glued (problems.cpp:21-61): the glued test matrix n x (num_panels *
+ * panel_width), bit-identical to the reference for the same arguments (the
+ * config-2 input).  n must be the context's global row count;
+ * the rank's rows [row_begin, row_end) go to out (device, column-major, ld
+ * ldo).  Gaussian drawn on the host with glibc as rng.hpp:37-49 does; the
+ * Householder QR's row-order dot products run on the device. */
+int bo_gen_glued(bo_ctx ctx, uint64_t n, uint64_t num_panels, uint64_t panel_width, double kappa_panel,
+                 double kappa_global, uint64_t seed, double* out, uint64_t ldo, bo_status* st);
 /* spmv (sparse.cpp:51-63): y = A x (local rows; x is the local shard, halo
  * exchanged internally when world > 1) */
 int bo_spmv(bo_op op, const double* x, double* y, bo_status* st);

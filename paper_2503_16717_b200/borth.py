@@ -711,6 +711,18 @@ def write_matrix_market(path, nrows: int, ncols: int, row_ptr, col, val):
           ci.ctypes.data_as(C.POINTER(C.c_int64)), _dp(vv))
 
 
+def gen_glued(ctx: Context, num_panels: int, panel_width: int, kappa_panel: float, kappa_global: float,
+              seed: int):
+    """gen_glued (problems.cpp:21-61) over the context's n global rows,
+    bit-identical to the reference; returns the rank's rows as a device panel
+    (num_panels * panel_width, ld)."""
+    out = ctx.panel(num_panels * panel_width, zero=False)
+    ctx.stream.synchronize()
+    _call(ctx.lib.bo_gen_glued, ctx.h, ctx.n, num_panels, panel_width, float(kappa_panel), float(kappa_global),
+          seed, _ptr(out), ctx.ld)
+    return out
+
+
 # -------------------------------------------------------------- operator --
 def convdiff_coeffs(w: float = 0.3):
     """7-point coefficients (i-1, j-1, l-1, self, l+1, j+1, i+1) of the config-5

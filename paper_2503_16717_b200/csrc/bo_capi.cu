@@ -17,8 +17,10 @@
 #include <cstdio>
 #include <cstring>
 #include <future>
+#include <map>
 #include <mutex>
 #include <random>
+#include <set>
 #include <unordered_map>
 
 #include "bo_internal.h"
@@ -56,18 +58,6 @@ void ok_st(bo_status* st) {
     st->msg[0] = 0;
   }
 }
-#define CU(call)                                                                            \
-  do {                                                                                      \
-    cudaError_t e_ = (call);                                                                \
-    if (e_ != cudaSuccess)                                                                  \
-      return set_st(st, BO_CUDA, 0, 0.0, "CUDA error %s at %s:%d", cudaGetErrorString(e_), \
-                    __FILE__, __LINE__);                                                    \
-  } while (0)
-#define TRY(expr)          \
-  do {                     \
-    int rc_ = (expr);      \
-    if (rc_ != BO_OK) return rc_; \
-  } while (0)
 
 
 // ---------------------------------------------------------------------------
@@ -341,13 +331,15 @@ int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st) {
 
   PassFn fn = get_pass_fn(nt, T, r.kind, r.exact, r.K);
   static std::mutex mu;
-  static std::unordered_map<const void*, size_t> attr_set;
+  // the opt-in is a per-device function attribute: key the cache on (device, fn)
+  static std::map<std::pair<int, const void*>, size_t> attr_set;
   {
     std::lock_guard<std::mutex> g(mu);
-    auto it = attr_set.find((const void*)fn);
+    const auto key = std::make_pair(ctx->device, (const void*)fn);
+    auto it = attr_set.find(key);
     if (it == attr_set.end() || it->second < total) {
       CU(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)total));
-      attr_set[(const void*)fn] = total;
+      attr_set[key] = total;
     }
   }
   cudaEvent_t pe0 = nullptr, pe1 = nullptr;
@@ -575,8 +567,10 @@ static int ctx_create_impl(int device, int rank, int world, const void* nccl_id,
   CU(cudaSetDevice(device));
   cudaDeviceProp prop;
   CU(cudaGetDeviceProperties(&prop, device));
-  if (prop.major < 10)
-    return set_st(st, BO_CUDA, 0, 0.0, "device %s (sm_%d%d) is not sm_100", prop.name, prop.major, prop.minor);
+  // built for sm_100a only: arch-specific features do not carry to sm_103 / sm_11x / sm_12x
+  if (prop.major != 10 || prop.minor != 0)
+    return set_st(st, BO_CUDA, 0, 0.0, "device %s (sm_%d%d) is not sm_100 (library built for sm_100a only)",
+                  prop.name, prop.major, prop.minor);
   bo_ctx c = new bo_ctx_s();
   c->device = device;
   c->rank = rank;
@@ -827,10 +821,14 @@ int gen_stream(bo_ctx ctx, uint64_t mt_seed, const std::vector<std::pair<uint64_
   ga.jidx_off = plan.dev + 2 * nc;
   ga.jidx = reinterpret_cast<const uint16_t*>(plan.dev + 3 * nc + 1);
   const size_t smem = (size_t)(kPrefixWords + 8 + kRing * kMtN + 2 * kRing) * 8;
-  static bool attr = false;
-  if (!attr) {
-    CU(cudaFuncSetAttribute((const void*)mt_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
+  static std::mutex attr_mu;
+  static std::set<int> attr_dev;  // per-device opt-in
+  {
+    std::lock_guard<std::mutex> g(attr_mu);
+    if (!attr_dev.count(ctx->device)) {
+      CU(cudaFuncSetAttribute((const void*)mt_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr_dev.insert(ctx->device);
+    }
   }
   mt_stream_kernel<<<(unsigned)nc, 1024, smem, ctx->stream>>>(ga);
   CU(cudaGetLastError());

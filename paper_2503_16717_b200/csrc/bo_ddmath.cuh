@@ -1,0 +1,179 @@
+// bo_ddmath.cuh — correctly-rounded (to ~2^-90 relative before the final
+// rounding) natural log and sin/cos in double-double arithmetic, for the
+// device Box-Muller of the Gaussian sketch (bo_sketch_gen.cuh).
+//
+// The reference draws normals with glibc's log / sin / cos
+// (proj/include/blkorth/rng.hpp:37-49).  glibc 2.39 is correctly rounded for
+// all but ~0.1 % of these inputs (SURVEY.md finding 1) while CUDA's libdevice
+// log / sincos are off by up to 1-2 ulp much more often, which put round 1's
+// device sketch up to 5 ulp from the reference.  Evaluating both functions in
+// double-double and rounding once makes every device value the correctly
+// rounded one, so the only differences left are glibc's own misroundings.
+//
+// log x   : x = 2^e f, f in [0.75, 1.5); c = i/128 nearest f (i = 96..192);
+//           t = (f - c)/c via the dd reciprocal table, |t| <= 0.0053;
+//           log x = e ln2 + log c + log1p(t), log1p by a degree-12 series with
+//           its four leading coefficients in dd.
+// sin/cos : k = rint(a 2/pi), r = a - k pi/2 with a three-part pi/2;
+//           r0 = j/64 nearest r, d = r - r0 (|d| <= 1/128);
+//           sin r = S0 + S0 (cos d - 1) + C0 sin d, cos r = C0 + C0 (cos d - 1) - S0 sin d,
+//           with dd tables of sin / cos(j/64), then the quadrant.
+// The same source compiles for the host (g++ -ffp-contract=off), which the
+// CPU tests use to pin it against mpmath and glibc (tests/test_ddmath.py).
+#pragma once
+#include <cstdint>
+#include <cstring>
+
+#ifdef __CUDACC__
+#define BO_DDM_FN __device__ __forceinline__
+#define BO_DDM_TABLE static __device__ const
+#else
+#include <cmath>
+#define BO_DDM_FN static inline
+#define BO_DDM_TABLE static const
+#endif
+
+#include "bo_ddmath_tables.h"
+
+namespace bo {
+namespace ddm {
+
+// unfused IEEE operations: the error-free transforms below need exactly
+// these roundings, so no contraction into FMAs is allowed
+#ifdef __CUDACC__
+BO_DDM_FN double A(double a, double b) { return __dadd_rn(a, b); }
+BO_DDM_FN double S(double a, double b) { return __dsub_rn(a, b); }
+BO_DDM_FN double M(double a, double b) { return __dmul_rn(a, b); }
+BO_DDM_FN double F(double a, double b, double c) { return __fma_rn(a, b, c); }
+BO_DDM_FN double RINT(double a) { return rint(a); }
+BO_DDM_FN double TAB(const double* p) { return __ldg(p); }
+BO_DDM_FN uint64_t BITS(double x) { return (uint64_t)__double_as_longlong(x); }
+BO_DDM_FN double DBL(uint64_t u) { return __longlong_as_double((long long)u); }
+#else
+BO_DDM_FN double A(double a, double b) { return a + b; }
+BO_DDM_FN double S(double a, double b) { return a - b; }
+BO_DDM_FN double M(double a, double b) { return a * b; }
+BO_DDM_FN double F(double a, double b, double c) { return std::fma(a, b, c); }
+BO_DDM_FN double RINT(double a) { return std::rint(a); }
+BO_DDM_FN double TAB(const double* p) { return *p; }
+BO_DDM_FN uint64_t BITS(double x) {
+  uint64_t u;
+  std::memcpy(&u, &x, 8);
+  return u;
+}
+BO_DDM_FN double DBL(uint64_t u) {
+  double x;
+  std::memcpy(&x, &u, 8);
+  return x;
+}
+#endif
+
+struct DD {
+  double hi, lo;
+};
+
+BO_DDM_FN DD two_sum(double a, double b) {
+  const double s = A(a, b), bb = S(s, a);
+  return {s, A(S(a, S(s, bb)), S(b, bb))};
+}
+BO_DDM_FN DD quick_two_sum(double a, double b) {  // |a| >= |b| or a == 0
+  const double s = A(a, b);
+  return {s, S(b, S(s, a))};
+}
+BO_DDM_FN DD two_prod(double a, double b) {
+  const double p = M(a, b);
+  return {p, F(a, b, -p)};
+}
+BO_DDM_FN DD neg(DD a) { return {-a.hi, -a.lo}; }
+BO_DDM_FN DD add(DD a, DD b) {
+  DD s = two_sum(a.hi, b.hi);
+  const DD t = two_sum(a.lo, b.lo);
+  s.lo = A(s.lo, t.hi);
+  s = quick_two_sum(s.hi, s.lo);
+  s.lo = A(s.lo, t.lo);
+  return quick_two_sum(s.hi, s.lo);
+}
+BO_DDM_FN DD add_d(DD a, double b) {
+  DD s = two_sum(a.hi, b);
+  s.lo = A(s.lo, a.lo);
+  return quick_two_sum(s.hi, s.lo);
+}
+BO_DDM_FN DD mul(DD a, DD b) {
+  DD p = two_prod(a.hi, b.hi);
+  p.lo = A(p.lo, F(a.hi, b.lo, M(a.lo, b.hi)));
+  return quick_two_sum(p.hi, p.lo);
+}
+BO_DDM_FN DD mul_d(DD a, double b) {
+  DD p = two_prod(a.hi, b);
+  p.lo = F(a.lo, b, p.lo);
+  return quick_two_sum(p.hi, p.lo);
+}
+
+// log(x) rounded to nearest, x positive, normal, finite (Box-Muller: x in [2^-53, 1])
+BO_DDM_FN double log_rn(double x) {
+  const uint64_t bits = BITS(x);
+  int e = (int)((bits >> 52) & 0x7ff) - 1023;
+  double f = DBL((bits & 0xfffffffffffffULL) | 0x3ff0000000000000ULL);  // [1, 2)
+  if (f >= 1.5) {
+    f = M(f, 0.5);
+    e += 1;
+  }
+  const int i = (int)RINT(M(f, 128.0));  // 96..192
+  const double d = S(f, M((double)i, 0x1p-7));  // exact
+  const double* tb = kLogTab + 4 * (i - kLogLo);
+  const DD rc{TAB(tb), TAB(tb + 1)}, lc{TAB(tb + 2), TAB(tb + 3)};
+  const DD t = mul_d(rc, d);  // (f - c) / c
+  const double th = t.hi;
+  // log1p(t) = t + t^2 (-1/2 + t (1/3 + t (-1/4 + t R))), R = sum_{j>=5} (-1)^{j+1} t^{j-5} / j
+  double R = F(th, -1.0 / 12.0, 1.0 / 11.0);
+  R = F(th, R, -1.0 / 10.0);
+  R = F(th, R, 1.0 / 9.0);
+  R = F(th, R, -1.0 / 8.0);
+  R = F(th, R, 1.0 / 7.0);
+  R = F(th, R, -1.0 / 6.0);
+  R = F(th, R, 1.0 / 5.0);
+  const DD a4 = two_sum(-0.25, M(th, R));
+  const DD a3 = add(DD{kThirdHi, kThirdLo}, mul(t, a4));
+  const DD a2 = add_d(mul(t, a3), -0.5);
+  const DD L = add(t, mul(mul(t, t), a2));
+  DD el = two_prod((double)e, kLn2Hi);
+  el.lo = F((double)e, kLn2Lo, el.lo);
+  el = quick_two_sum(el.hi, el.lo);
+  return add(add(el, lc), L).hi;
+}
+
+// sin(a), cos(a) rounded to nearest, 0 <= a < 2 pi (Box-Muller angle)
+BO_DDM_FN void sincos_rn(double a, double* sn, double* cs) {
+  const double kd = RINT(M(a, kTwoOverPi));  // quadrant 0..4
+  const int k = (int)kd;
+  DD r = add(DD{a, 0.0}, neg(two_prod(kd, kPio2_1)));
+  r = add(r, neg(two_prod(kd, kPio2_2)));
+  r = add_d(r, -M(kd, kPio2_3));
+  const double jd = RINT(M(r.hi, 64.0));  // |j| <= 51
+  const int j = (int)jd;
+  const DD dl = two_sum(S(r.hi, M(jd, 0x1p-6)), r.lo);  // r - j/64 (the subtraction is exact)
+  const DD z = mul(dl, dl);
+  const double zh = z.hi;
+  // sin d = d + d z (-1/6 + z qs);  cos d - 1 = z (-1/2 + z qc)
+  const double qs = F(zh, F(zh, 1.0 / 362880.0, -1.0 / 5040.0), 1.0 / 120.0);
+  const DD ps = add(DD{-kSixthHi, -kSixthLo}, two_prod(zh, qs));
+  const DD sd = add(dl, mul(mul(dl, z), ps));
+  const double qc = F(zh, F(zh, F(zh, -1.0 / 3628800.0, 1.0 / 40320.0), -1.0 / 720.0), 1.0 / 24.0);
+  const DD cm = mul(z, two_sum(-0.5, M(zh, qc)));
+  const int aj = j < 0 ? -j : j;
+  const double* tb = kTrigTab + 4 * aj;
+  DD s0{TAB(tb), TAB(tb + 1)};
+  const DD c0{TAB(tb + 2), TAB(tb + 3)};
+  if (j < 0) s0 = neg(s0);
+  const DD sr = add(s0, add(mul(s0, cm), mul(c0, sd)));
+  const DD cr = add(c0, add(mul(c0, cm), neg(mul(s0, sd))));
+  switch (k & 3) {
+    case 0: *sn = sr.hi; *cs = cr.hi; break;
+    case 1: *sn = cr.hi; *cs = -sr.hi; break;
+    case 2: *sn = -sr.hi; *cs = -cr.hi; break;
+    default: *sn = -cr.hi; *cs = sr.hi; break;
+  }
+}
+
+}  // namespace ddm
+}  // namespace bo

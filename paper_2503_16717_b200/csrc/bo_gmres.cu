@@ -21,18 +21,6 @@
 using namespace bo;
 using namespace bo::host;
 
-#define CU(call)                                                                            \
-  do {                                                                                      \
-    cudaError_t e_ = (call);                                                                \
-    if (e_ != cudaSuccess)                                                                  \
-      return set_st(st, BO_CUDA, 0, 0.0, "CUDA error %s at %s:%d", cudaGetErrorString(e_), \
-                    __FILE__, __LINE__);                                                    \
-  } while (0)
-#define TRY(expr)                 \
-  do {                            \
-    int rc_ = (expr);             \
-    if (rc_ != BO_OK) return rc_; \
-  } while (0)
 
 namespace bo {
 
@@ -392,7 +380,7 @@ int diagnostics(Gm& g, bo_basis b, const hd::Mat& H, size_t q_in, double a_fro, 
   bo_ctx ctx = g.ctx;
   const size_t p = b->cols;
   *orth = 0.0;
-  if (p > 0 && p <= 64) {
+  if (p > 0) {  // any width: the Gram is assembled from 64 x 64 blocks
     std::vector<double> G;
     TRY(wide_gram_host(ctx, b->q, ctx->ld, (int)p, G, st));
     std::vector<double> a(p * p);
@@ -468,6 +456,12 @@ extern "C" int bo_sstep_gmres(bo_op op, const double* b, const double* x0, const
   if (cfg->shat % cfg->s != 0) return set_st(st, BO_INVALID, 0, 0.0, "s must divide shat");
   if (cfg->m % cfg->shat != 0) return set_st(st, BO_INVALID, 0, 0.0, "shat must divide m");
   if (op->ncols != ctx->n_global) return set_st(st, BO_INVALID, 0, 0.0, "coefficient matrix must be square");
+  // engine limits (not reference limits): the x-update / Arnoldi kernels stage
+  // y and h columns of up to 256 entries in shared memory, and the two-stage
+  // big panel (shat + 1 columns) goes through the <= 64-column wide passes
+  if (cfg->m + 1 > 256) return set_st(st, BO_INVALID, 0, 0.0, "m + 1 > 256 is not supported by the GPU driver");
+  if ((cfg->scheme == BO_TWOSTAGE_PIP || cfg->scheme == BO_TWOSTAGE_RANDBCGS) && cfg->shat + 1 > 64)
+    return set_st(st, BO_INVALID, 0, 0.0, "two-stage big panel shat + 1 > 64 columns is not supported by the GPU engine");
   if (cfg->n != 0 && cfg->n != ctx->n_global) return set_st(st, BO_INVALID, 0, 0.0, "config n does not match the matrix dimension");
   if (cfg->s + 1 > 16) return set_st(st, BO_INVALID, 0, 0.0, "s > 15 is outside the streaming-pass engine");
   const uint64_t n = ctx->n_global, nl = ctx->n_local, ld = ctx->ld;
@@ -591,7 +585,7 @@ extern "C" int bo_sstep_gmres(bo_op op, const double* b, const double* x0, const
                          : bo_bcgs2(store, panel, ld, K,
                                     cfg->scheme == BO_BCGS2_CHOLQR2 ? BO_INTRA_CHOLQR2 : BO_INTRA_RAND_CHOLQR, theta,
                                     overlap, &pst);
-      if (prc == BO_CUDA || prc == BO_NCCL) {
+      if (prc == BO_CUDA || prc == BO_NCCL || prc == BO_INVALID) {  // not a numerical breakdown
         if (st) *st = pst;
         return prc;
       }
@@ -606,7 +600,7 @@ extern "C" int bo_sstep_gmres(bo_op op, const double* b, const double* x0, const
       if (twostage && !cs.happy && !cs.aborted && (j + 1) % ppb == 0) {
         bo_status fst;
         int frc = bo_two_stage_finish(store, preproc, cfg->reorthogonalize, 0, nullptr, &fst);
-        if (frc == BO_CUDA || frc == BO_NCCL) {
+        if (frc == BO_CUDA || frc == BO_NCCL || frc == BO_INVALID) {
           if (st) *st = fst;
           return frc;
         }
@@ -620,7 +614,7 @@ extern "C" int bo_sstep_gmres(bo_op op, const double* b, const double* x0, const
     if (twostage && cs.aborted && store->cols > store->bp_lo && store->cols > 0) {
       bo_status fst;
       int frc = bo_two_stage_finish(store, preproc, cfg->reorthogonalize, 0, nullptr, &fst);
-      if (frc == BO_CUDA || frc == BO_NCCL) {
+      if (frc == BO_CUDA || frc == BO_NCCL || frc == BO_INVALID) {
         if (st) *st = fst;
         return frc;
       }

@@ -205,6 +205,19 @@ constexpr int kNcclUint64 = 5;   // ncclUint64
 constexpr int kNcclSum = 0;
 
 int set_st(bo_status* st, int code, long long index, double pivot, const char* fmt, ...);
+// return BO_CUDA with the error text from a bo_status*-returning function
+#define CU(call)                                                                            \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return set_st(st, BO_CUDA, 0, 0.0, "CUDA error %s at %s:%d", cudaGetErrorString(e_), \
+                    __FILE__, __LINE__);                                                    \
+  } while (0)
+#define TRY(expr)                 \
+  do {                            \
+    int rc_ = (expr);             \
+    if (rc_ != BO_OK) return rc_; \
+  } while (0)
 void ok_st(bo_status* st);
 int run_pass(bo_ctx ctx, PassReq& r, bo_status* st);        // splits p > 64 into chunks
 int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st);

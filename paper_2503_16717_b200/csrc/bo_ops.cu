@@ -26,18 +26,6 @@
 using namespace bo;
 using namespace bo::host;
 
-#define CU(call)                                                                            \
-  do {                                                                                      \
-    cudaError_t e_ = (call);                                                                \
-    if (e_ != cudaSuccess)                                                                  \
-      return set_st(st, BO_CUDA, 0, 0.0, "CUDA error %s at %s:%d", cudaGetErrorString(e_), \
-                    __FILE__, __LINE__);                                                    \
-  } while (0)
-#define TRY(expr)                 \
-  do {                            \
-    int rc_ = (expr);             \
-    if (rc_ != BO_OK) return rc_; \
-  } while (0)
 
 namespace bo {
 
@@ -1318,11 +1306,23 @@ extern "C" int bo_two_stage_finish(bo_basis b, int preproc, int reorthogonalize,
 
 namespace bo {
 namespace host {
-// Gram of p <= 64 device columns, summed over ranks, to host (p x p)
+// Gram of p device columns, summed over ranks, to host (p x p, column-major),
+// assembled from 64 x 64 blocks (upper blocks computed, lower mirrored)
 int wide_gram_host(bo_ctx ctx, const double* q, uint64_t ld, int p, std::vector<double>& G, bo_status* st) {
-  hd::Mat M;
-  TRY(wide_contract(ctx, q, ld, p, q, ld, p, M, st));
-  G = M.a;
+  G.assign((size_t)p * p, 0.0);
+  for (int j0 = 0; j0 < p; j0 += 64) {
+    const int nj = std::min(64, p - j0);
+    for (int i0 = 0; i0 <= j0; i0 += 64) {
+      const int ni = std::min(64, p - i0);
+      hd::Mat M;
+      TRY(wide_contract(ctx, q + (size_t)i0 * ld, ld, ni, q + (size_t)j0 * ld, ld, nj, M, st));
+      for (int j = 0; j < nj; ++j)
+        for (int i = 0; i < ni; ++i) {
+          G[(size_t)(i0 + i) + (size_t)(j0 + j) * p] = M(i, j);
+          G[(size_t)(j0 + j) + (size_t)(i0 + i) * p] = M(i, j);
+        }
+    }
+  }
   return BO_OK;
 }
 }  // namespace host

@@ -9,11 +9,12 @@
 // g[J+t] = XOR_{k in p} g[k+t], p = x^J mod phi (host-computed, mt64_jump.cpp),
 // with the 20248-word stream prefix held in shared memory, then twists
 // 312-word windows and tempers/transforms each word (mt_stream_kernel).
-// Count (bucket, sign) is bit-identical to the reference; Gaussian values use
-// the device libm log/sin/cos (<= 1-2 ulp from glibc's).
+// Count (bucket, sign) is bit-identical to the reference; Gaussian values are
+// the reference formula with correctly rounded log / sin / cos (bo_ddmath.cuh).
 #pragma once
 #include <cstdint>
 
+#include "bo_ddmath.cuh"
 #include "bo_ptx.cuh"
 #include "bo_tiny.cuh"
 
@@ -75,10 +76,12 @@ __device__ __forceinline__ void gen_transform(const GenArgs& a, const uint64_t* 
     // rng.hpp:37-49 (normal #q = r cos, #q+1 = r sin)
     const double u1 = ((double)(y0 >> 11) + 1.0) * 0x1.0p-53;
     const double u2 = (double)(y1 >> 11) * 0x1.0p-53;
-    const double rr = sqrt(tiny::mul(-2.0, log(u1)));
+    // correctly rounded log / sin / cos (bo_ddmath.cuh): the only differences
+    // from the reference left are glibc's own misroundings (~0.1 % of inputs)
+    const double rr = sqrt(tiny::mul(-2.0, ddm::log_rn(u1)));
     const double ang = tiny::mul(6.283185307179586476925286766559, u2);
     double sn, cs;
-    sincos(ang, &sn, &cs);
+    ddm::sincos_rn(ang, &sn, &cs);
     const double v0 = tiny::mul(a.scale, tiny::mul(rr, cs));
     const double v1 = tiny::mul(a.scale, tiny::mul(rr, sn));
     uint64_t c1 = col, r1 = row + 1;

@@ -40,6 +40,32 @@ def gpu():
     return P
 
 
+@pytest.fixture(scope="session")
+def ddm_host():
+    """host build of the device double-double log / sincos (tests/native/ddmath_host.cpp)"""
+    import ctypes as C
+    src = ROOT / "tests" / "native" / "ddmath_host.cpp"
+    hdrs = [ROOT / "paper_2503_16717_b200" / "csrc" / h for h in ("bo_ddmath.cuh", "bo_ddmath_tables.h")]
+    so = ROOT / "tests" / "native" / "libddm_host.so"
+    if not so.exists() or any(p.stat().st_mtime > so.stat().st_mtime for p in [src, *hdrs]):
+        import subprocess
+        subprocess.run(["g++", "-O2", "-ffp-contract=off", "-fPIC", "-shared", str(src), "-o", str(so)], check=True)
+    lib = C.CDLL(str(so))
+    dp = C.POINTER(C.c_double)
+    for name in ("ddm_log_n", "glibc_log_n"):
+        getattr(lib, name).argtypes = [dp, dp, C.c_long]
+    for name in ("ddm_sincos_n", "glibc_sincos_n"):
+        getattr(lib, name).argtypes = [dp, dp, dp, C.c_long]
+    lib.box_muller_n.argtypes = [C.c_uint64, C.c_long, C.c_int, dp]
+    lib.theta_cr.argtypes = [C.c_uint64, C.c_long, C.c_long, dp]
+    return lib
+
+
+def ulps(a, b):
+    """|a - b| in units in the last place (same-sign finite doubles)"""
+    return np.abs(np.asarray(a, dtype=np.float64).view(np.int64) - np.asarray(b, dtype=np.float64).view(np.int64))
+
+
 def rel_err(a, b):
     a, b = np.asarray(a), np.asarray(b)
     den = max(np.max(np.abs(b)), 1e-300)
