@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--no-gmres", action="store_true", help="skip the C3 GMRES time/restart leg")
     ap.add_argument("--gmres-restarts", type=int, default=3)
     ap.add_argument("--cpu-rows", type=int, default=1 << 18)
+    ap.add_argument("--ref-cores", type=int, default=0, help="--impl reference: cap on host cores (0 = all usable)")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu")
     ap.add_argument("--comm", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: collectives through torch.distributed gloo (bo_ctx_create_comm), every rank on "
@@ -121,14 +122,49 @@ def measured_peak():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+# ------------------------------------------------------------------ config --
+def host_cpu():
+    """CPU model and core counts of this host"""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"model": model, "logical_cpus": os.cpu_count(), "usable_cpus": len(os.sched_getaffinity(0))}
+
+
+def workload_config(args, world):
+    """the `config` both arms print (identical for --impl ours / reference)"""
+    k = args.s + 1
+    ps = [p * k for p in range(args.panels)]
+    return {"workload": f"C2 microbench: bcgs2 + {args.intra}, gen_glued({args.n}, {args.panels}, {k}, "
+                        f"{args.kappa:g}, {args.kappa:g}, 7) (problems.cpp:21-61), s={args.s} (k={k}), "
+                        f"{args.panels} calls p=0..{ps[-1]}, {args.sketch} sketch mhat={2 * k} seed 1",
+            "n_rows": args.n, "s": args.s, "panels": args.panels, "intra": args.intra, "kappa": args.kappa,
+            "parallelism": f"row-shard x{world}",
+            "l2": "inputs (%.1f GB/step) larger than L2 (126 MB); no flush" % (8 * args.n * k * args.panels / 1e9),
+            "algo_words_per_row": algo_words_per_row(ps, k)}
+
+
 # --------------------------------------------------------------- reference --
-def cpu_reference_sequence(n, k, panels, intra, kappa, reps=1):
-    """The unmodified reference (oracle/_ref, compiled from /root/reference
-    sources) timed on one host core: same 6-call bcgs2 sequence at n rows."""
+def _ref_oracle():
     sys.path.insert(0, str(ROOT / "oracle"))
     from py_oracle import Oracle, have_ref
     which = "ref" if have_ref() else "orc"
-    o = Oracle(which)
+    return which, Oracle(which)
+
+
+def cpu_reference_sequence(n, k, panels, intra, kappa, reps=1, core=None):
+    """The unmodified reference (oracle/_ref, compiled from /root/reference
+    sources) on one host core (pinned): the same 6-call bcgs2 sequence on its
+    own gen_glued(n, panels, k, kappa, kappa, 7) input, n = the sample rows.
+    Returns (which, best seconds)."""
+    if core is not None:
+        os.sched_setaffinity(0, {core})
+    which, o = _ref_oracle()
     v = o.gen_glued(n, panels, k, kappa, kappa, 7)
     sk = o.sketch_build(0, n, k - 1, 1).h if intra == 1 else None
     times = []
@@ -143,67 +179,105 @@ def cpu_reference_sequence(n, k, panels, intra, kappa, reps=1):
     return which, min(times)
 
 
+def _ref_worker(core, n, k, panels, intra, kappa, steps, barrier, out):
+    """one reference process pinned to `core`: its own row shard of n rows,
+    one timed sequence per step (between barriers)"""
+    os.sched_setaffinity(0, {core})
+    which, o = _ref_oracle()
+    v = o.gen_glued(n, panels, k, kappa, kappa, 7)
+    sk = o.sketch_build(0, n, k - 1, 1).h if intra == 1 else None
+    ts = []
+    for _ in range(steps):
+        barrier.wait()
+        b = o.basis_new(n, panels * k)
+        t0 = time.perf_counter()
+        for p in range(panels):
+            r = o.bcgs2(b, v[:, p * k:(p + 1) * k], intra, sk)
+            assert r.code == 0, r.msg
+        ts.append(time.perf_counter() - t0)
+        o.basis_free(b)
+    out.put((core, which, ts))
+
+
 def run_reference_arm(args):
-    """--impl reference: the reference CPU implementation on the host cores
-    (single-threaded by design, proj/include/blkorth/dense.hpp:121-122)."""
+    """--impl reference: the reference CPU implementation (single-threaded by
+    design, proj/include/blkorth/dense.hpp:121-122) on ALL usable host cores:
+    one pinned process per core, each running the reference's bcgs2 sequence
+    on its own cpu_rows-row shard (its own gen_glued input).  That is the
+    reference's throughput with every core busy and no reductions between
+    shards (an upper bound for a distributed CPU run).  Rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    import multiprocessing as mp
     k = args.s + 1
     intra = 1 if args.intra == "rand_cholqr" else 0
-    ps = [p * k for p in range(args.panels)]
-    words = algo_words_per_row(ps, k)
+    words = algo_words_per_row([p * k for p in range(args.panels)], k)
     n = args.cpu_rows
-    for _ in range(max(args.warmup, 0) and 1):
-        cpu_reference_sequence(n, k, args.panels, intra, args.kappa, 1)
-    tot = 0.0
-    which = "ref"
-    for _ in range(args.steps):
-        which, t = cpu_reference_sequence(n, k, args.panels, intra, args.kappa, 1)
-        tot += t
-    sec = tot / max(args.steps, 1)
-    gbs = 8.0 * n * words / sec / 1e9
+    cores = sorted(os.sched_getaffinity(0))[:128]
+    if args.ref_cores:
+        cores = cores[: args.ref_cores]
+    steps = max(args.steps, 1) + max(args.warmup, 0)
+    ctxm = mp.get_context("fork")
+    barrier = ctxm.Barrier(len(cores))
+    q = ctxm.Queue()
+    procs = [ctxm.Process(target=_ref_worker, args=(c, n, k, args.panels, intra, args.kappa, steps, barrier, q))
+             for c in cores]
+    for pr in procs:
+        pr.start()
+    res = [q.get() for _ in procs]
+    for pr in procs:
+        pr.join()
+    which = res[0][1]
+    w = max(args.warmup, 0)
+    per_step = [max(r[2][i] for r in res) for i in range(w, steps)]  # slowest core per step
+    sec = sum(per_step) / len(per_step)
+    gbs = len(cores) * 8.0 * n * words / sec / 1e9
+    one = sum(sum(r[2][w:]) / len(r[2][w:]) for r in res) / len(res)
     out = {
         "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (gen_glued, kappa=%g)" % args.kappa,
-        "config": {"workload": "C2 bcgs2 sequence (p=0..%d, k=%d) on a %d-row sample of the 8e6-row workload"
-                   % (ps[-1], k, n), "n_rows_sample": n, "s": args.s, "panels": args.panels, "intra": args.intra},
-        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": 1,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference gen_glued, same generator and arguments, cpu_rows-row shards)",
+        "config": workload_config(args, args.gpus),
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": len(cores),
                          "kind": "reference" if which == "ref" else "port",
-                         "sample": f"{n} rows x {args.panels} panels, one sequence per step"},
+                         "sample": f"{len(cores)} pinned processes x {n} rows x {args.panels} panels "
+                                   f"(gen_glued({n}, {args.panels}, {k}, {args.kappa:g}, {args.kappa:g}, 7) each), "
+                                   f"one sequence per process per step; step time = slowest process",
+                         "single_core_gbs": 8.0 * n * words / one / 1e9, "host": host_cpu()},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
 
 
 # --------------------------------------------------------------------- ours --
-def make_panels(P, ctx, torch, n_global, k, panels, kappa_panel, kappa_global, seed):
-    """Synthetic glued-style panels (problems.cpp:21-61 structure): V_p = U_p
-    diag(sigma_p) W_p^T with U orthonormal (Gaussian panels orthonormalised by
-    this library's own BCGS2) and W_p random orthogonal; sigma log-spaced."""
-    total = panels * k
-    g = torch.Generator(device=ctx.device)
-    g.manual_seed(1000 + seed * 7919 + ctx.rank)
-    st = P.BasisStore(ctx, total)
-    for p in range(panels):
-        raw = torch.randn((k, ctx.ld), generator=g, device=ctx.device, dtype=torch.float64)
-        raw[:, ctx.n_local:] = 0
-        P.bcgs2(st, raw, P.borth.CHOLQR2)
-    U = st.q_device().clone()
-    st.close()
-    rs = np.random.default_rng(seed)
-    span = max(kappa_global / kappa_panel, 1.0)
-    out = []
-    for p in range(panels):
-        scale = 1.0 if panels == 1 else span ** (-p / (panels - 1))
-        sig = np.array([scale * (kappa_panel ** (-c / (k - 1)) if k > 1 else 1.0) for c in range(k)])
-        w, _ = np.linalg.qr(rs.standard_normal((k, k)))
-        M = torch.from_numpy((np.diag(sig) @ w.T)).to(ctx.device)  # V^T = M^T U_p^T
-        vp = (M.T @ U[p * k:(p + 1) * k]).contiguous()
-        out.append(vp)
-    del U
-    return out
+def make_panels(P, ctx, args):
+    """The C2 input: gen_glued(n, panels, k, kappa, kappa, 7) (problems.cpp:21-61)
+    from the device generator, bit-identical to the reference's
+    (tests/test_gpu_c2_full.py pins it by sha256); each rank keeps its rows."""
+    k = args.s + 1
+    v = P.gen_glued(ctx, args.panels, k, args.kappa, args.kappa, 7)
+    return [v[p * k:(p + 1) * k] for p in range(args.panels)]
+
+
+def golden_big():
+    p = ROOT / "tests" / "golden" / "reference_big.json"
+    return json.loads(p.read_text()) if p.exists() else {}
+
+
+def gmres_parity(rep, want):
+    """the bench run's GMRES outcome against the reference's run of the same
+    configuration (tests/golden/reference_big.json)"""
+    if not want:
+        return None
+    n = min(len(rep["restart_relres"]), len(want["relres"]))
+    return {"restarts_match": rep["restarts"] == want["restarts"],
+            "iterations_match": rep["iterations"] == want["iterations"],
+            "ledger_match": rep["reduce"] == want["reduce"],
+            "relres_max_rel_delta": max((abs(a - b) / abs(b) for a, b in
+                                         zip(rep["restart_relres"][:n], want["relres"][:n])), default=None),
+            "reference": "tests/golden/reference_big.json (oracle/_ref)"}
 
 
 def main():
@@ -256,7 +330,9 @@ def main():
     ctx = make_ctx(n, rb, re_)
     intra = P.borth.RAND_CHOLQR if args.intra == "rand_cholqr" else P.borth.CHOLQR2
     torch.cuda.set_stream(ctx.stream)  # all torch work of this script on the library stream
-    panels = make_panels(P, ctx, torch, n, k, args.panels, args.kappa, args.kappa, 7)
+    t_gen = time.perf_counter()
+    panels = make_panels(P, ctx, args)
+    t_gen = time.perf_counter() - t_gen
     theta = P.SketchOperator.build(ctx, args.sketch, n, args.s, 1) if intra == P.borth.RAND_CHOLQR else None
     store = P.BasisStore(ctx, args.panels * k)
     ps = [p * k for p in range(args.panels)]
@@ -439,6 +515,8 @@ def main():
                  "relres": rep["restart_relres"], "reduce": rep["reduce"],
                  "phase_ms_per_restart": {kk: v / nr for kk, v in rep["t_ms"].items()},
                  "gpu_launches": launches_g,
+                 "parity": gmres_parity(rep, golden_big().get("c3_200")) if n == 8_000_000 and args.s == 10
+                 and rep["restarts"] == 4 else None,
                  "orth_gb_per_restart": 8.0 * n * algo_words_per_row([10 * j for j in range(60 // args.s)], args.s + 1) / 1e9}
         del op, bvec, x0
 
@@ -482,7 +560,8 @@ def main():
                           f"convection-diffusion {side5}^3 = {n5} rows ({ctx5.n_local} per GPU)",
               "ms_per_restart": rep5["t_ms"]["cycles"] / nr5, "ms_solve": m5, "restarts": rep5["restarts"],
               "iterations": rep5["iterations"], "relres": rep5["restart_relres"], "reduce": rep5["reduce"],
-              "phase_ms_per_restart": {kk: v / nr5 for kk, v in rep5["t_ms"].items()}}
+              "phase_ms_per_restart": {kk: v / nr5 for kk, v in rep5["t_ms"].items()},
+              "parity": gmres_parity(rep5, golden_big().get("c5_200")) if n5 == 8_000_000 else None}
         del op5, b5, x05
         if ctx5 is not ctx:
             ctx5.close()
@@ -499,14 +578,32 @@ def main():
             dist.all_reduce(gq)
     orth = float(torch.linalg.matrix_norm(torch.eye(gq.shape[0], device=gq.device, dtype=gq.dtype) - gq, ord=2))
 
+    # ---- C2 parity: the final R against the reference's run on the same input
+    c2_parity = None
+    gold = ROOT / "tests" / "golden" / "c2_ref.npz"
+    case = f"k{args.kappa:g}_{'randcholqr' if intra == P.borth.RAND_CHOLQR else 'cholqr2'}"
+    if gold.exists() and n == 8_000_000 and args.s == 10 and args.panels == 6 and args.sketch == "gaussian":
+        d = np.load(gold)
+        if case + "_R" in d:
+            R = store.r_copy()
+            Rw = d[case + "_R"]
+            c2_parity = {"case": case, "R_max_rel_err": float(np.max(np.abs(R - Rw)) / np.max(np.abs(Rw))),
+                         "ledger": store.ledger().counts,
+                         "reference_ledger": json.loads(str(d["meta"]))[case]["ledger"],
+                         "reference": "tests/golden/c2_ref.npz (oracle/_ref on the same gen_glued bytes)"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            which, sec = cpu_reference_sequence(args.cpu_rows, k, args.panels, intra, args.kappa, 2)
+            aff = os.sched_getaffinity(0)
+            core = sorted(aff)[0]
+            which, sec = cpu_reference_sequence(args.cpu_rows, k, args.panels, intra, args.kappa, 2, core=core)
+            os.sched_setaffinity(0, aff)
             cpu = {"value": 8.0 * args.cpu_rows * words / sec / 1e9, "unit": "GB/s", "cores": 1,
                    "kind": "reference" if which == "ref" else "port",
-                   "sample": f"{args.cpu_rows} rows x {args.panels} panels (one {args.intra} sequence, best of 2), "
-                             f"host core of the GPU box"}
+                   "sample": f"gen_glued({args.cpu_rows}, {args.panels}, {k}, {args.kappa:g}, {args.kappa:g}, 7): "
+                             f"one {args.intra} sequence (best of 2) on host core {core} (pinned)",
+                   "host": host_cpu()}
         except Exception as ex:  # pragma: no cover
             cpu = {"value": None, "unit": "GB/s", "cores": 1, "kind": "reference", "sample": f"failed: {ex}"}
 
@@ -515,13 +612,10 @@ def main():
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64",
-            "data": f"synthetic glued-style panels (kappa={args.kappa:g}), Gaussian sketch seed 1",
-            "config": {"workload": f"C2 microbench: {args.intra} BCGS2, n={n} rows, s={args.s} (k={k}), "
-                                   f"{args.panels} panels p=0..{ps[-1]}, sketch {args.sketch} mhat={2 * k}",
-                       "n_rows": n, "s": args.s, "panels": args.panels, "intra": args.intra,
-                       "parallelism": f"row-shard x{world}",
-                       "l2": "inputs (%.1f GB/step) larger than L2 (126 MB); no flush" % (8 * n * k * args.panels / 1e9),
-                       "algo_words_per_row": words},
+            "data": f"synthetic: reference gen_glued panels (device generator, bit-identical; "
+                    f"{t_gen:.1f} s setup), Gaussian sketch seed 1",
+            "config": workload_config(args, world),
+            "c2_parity": c2_parity,
             "roofline": {"bound": "hbm", "kernel": f"pass_kernel {top_kind} (p={top_p})", "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": top["bytes"], "ms_per_launch": top_ms,

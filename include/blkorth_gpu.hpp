@@ -19,17 +19,80 @@
 
 #include <array>
 #include <cstdint>
+#include <cstdio>
 #include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
 #include "bo_cuda.h"
+#if defined(BLKORTH_GPU_REFERENCE_TYPES)
+#include "blkorth/dense.hpp"
+#include "blkorth/errors.hpp"
+#endif
 
 namespace blkorth {
 namespace gpu {
 
-// ---- exceptions mirroring proj/include/blkorth/errors.hpp ------------------
+// CUDA / NCCL faults are not numerical breakdowns: they derive from
+// std::runtime_error only, so the reference driver's `catch (const Error&)`
+// (gmres.cpp:429-435) never routes them into recover_panel.
+struct DeviceError : std::runtime_error {
+  explicit DeviceError(const std::string& m) : std::runtime_error(m) {}
+};
+
+#if defined(BLKORTH_GPU_REFERENCE_TYPES)
+// ---- built against /root/reference/proj/include: the reference's own types.
+// Every library status is rethrown as the reference exception, constructed
+// with the reference's arguments, so what() is the reference text
+// (errors.hpp:12-92) and `catch (const blkorth::Error&)` sees it.
+using ::blkorth::AllColumnsDiscarded;
+using ::blkorth::AmbientTooSmall;
+using ::blkorth::BannerError;
+using ::blkorth::CholeskyBreakdown;
+using ::blkorth::Error;
+using ::blkorth::InvalidScheme;
+using ::blkorth::ParseError;
+using ::blkorth::RankDeficient;
+using ::blkorth::ReduceLedger;
+using ::blkorth::ReducePhase;
+using ::blkorth::SingularTriangular;
+using ::blkorth::UpperTriangular;
+using ::blkorth::ZeroMatrix;
+
+inline std::string after(const std::string& m, const std::string& prefix) {
+  return m.compare(0, prefix.size(), prefix) == 0 ? m.substr(prefix.size()) : m;
+}
+
+inline void check(int rc, const bo_status& st) {
+  if (rc == BO_OK) return;
+  const std::string m(st.msg);
+  switch (rc) {
+    case BO_CHOLESKY_BREAKDOWN: {  // "<context>: nonpositive Cholesky pivot at step <k>"
+      const std::size_t at = m.find(": nonpositive Cholesky pivot");
+      throw CholeskyBreakdown((std::size_t)st.index, at == std::string::npos ? m : m.substr(0, at));
+    }
+    case BO_SINGULAR_TRIANGULAR: throw SingularTriangular((std::size_t)st.index);
+    case BO_AMBIENT_TOO_SMALL: {
+      unsigned long long n = 0, mh = 0;
+      std::sscanf(st.msg, "ambient dimension n=%llu must exceed sketch size mhat=%llu", &n, &mh);
+      throw AmbientTooSmall((std::size_t)n, (std::size_t)mh);
+    }
+    case BO_ALL_COLUMNS_DISCARDED: throw AllColumnsDiscarded();
+    case BO_RANK_DEFICIENT: throw RankDeficient(m);
+    case BO_ZERO_MATRIX: throw ZeroMatrix();
+    case BO_INVALID: throw InvalidScheme(m);
+    case BO_PARSE_ERROR: {
+      const std::string tail = after(m, "parse error at line ");
+      const std::size_t colon = tail.find(": ");
+      throw ParseError((std::size_t)st.index, colon == std::string::npos ? tail : tail.substr(colon + 2));
+    }
+    case BO_BANNER_ERROR: throw BannerError(after(m, "unsupported MatrixMarket banner: "));
+    default: throw DeviceError(m);
+  }
+}
+#else
+// ---- standalone: exceptions mirroring proj/include/blkorth/errors.hpp ------
 struct Error : std::runtime_error {
   explicit Error(const std::string& m) : std::runtime_error(m) {}
 };
@@ -48,7 +111,8 @@ struct RankDeficient : Error { using Error::Error; };
 struct AllColumnsDiscarded : Error { using Error::Error; };
 struct ZeroMatrix : Error { using Error::Error; };
 struct InvalidScheme : Error { using Error::Error; };
-struct DeviceError : Error { using Error::Error; };
+struct ParseError : Error { using Error::Error; };
+struct BannerError : Error { using Error::Error; };
 
 inline void check(int rc, const bo_status& st) {
   if (rc == BO_OK) return;
@@ -61,6 +125,8 @@ inline void check(int rc, const bo_status& st) {
     case BO_RANK_DEFICIENT: throw RankDeficient(m);
     case BO_ZERO_MATRIX: throw ZeroMatrix(m);
     case BO_INVALID: throw InvalidScheme(m);
+    case BO_PARSE_ERROR: throw ParseError(m);
+    case BO_BANNER_ERROR: throw BannerError(m);
     default: throw DeviceError(m);
   }
 }
@@ -69,8 +135,28 @@ inline void check(int rc, const bo_status& st) {
 enum class ReducePhase : int { projection = 0, gram = 1, sketch = 2, norm = 3 };
 struct ReduceLedger {
   std::array<uint64_t, 4> counts{};
+  void record(ReducePhase p) { ++counts[(int)p]; }
   uint64_t count(ReducePhase p) const { return counts[(int)p]; }
   uint64_t total() const { return counts[0] + counts[1] + counts[2] + counts[3]; }
+};
+#endif
+
+// The C ABI counts ledger events in a uint64_t[4]; LedgerIO lends one to a call
+// and records the events it added into the caller's ReduceLedger.
+class LedgerIO {
+ public:
+  explicit LedgerIO(ReduceLedger& l) : l_(l) {
+    for (int p = 0; p < 4; ++p) c_[p] = c0_[p] = l.count((ReducePhase)p);
+  }
+  ~LedgerIO() {
+    for (int p = 0; p < 4; ++p)
+      for (uint64_t d = c0_[p]; d < c_[p]; ++d) l_.record((ReducePhase)p);
+  }
+  uint64_t* data() { return c_; }
+
+ private:
+  ReduceLedger& l_;
+  uint64_t c_[4], c0_[4];
 };
 
 enum class SketchKind { gaussian = BO_SKETCH_GAUSSIAN, count = BO_SKETCH_COUNT, count_gauss = BO_SKETCH_COUNT_GAUSS };
@@ -125,7 +211,7 @@ class SketchOperator {
   HostMatrix apply(const DevicePanel& v, ReduceLedger& ledger) const {
     HostMatrix out{sketch_size(), v.cols, std::vector<double>(sketch_size() * v.cols)};
     bo_status st{};
-    check(bo_sketch_apply(h_, v.data, v.ld, v.cols, out.a.data(), ledger.counts.data(), &st), st);
+    check(bo_sketch_apply(h_, v.data, v.ld, v.cols, out.a.data(), LedgerIO(ledger).data(), &st), st);
     return out;
   }
   bo_sketch get() const { return h_; }
@@ -143,20 +229,20 @@ struct QrResult {
 inline QrResult cholqr(Context& c, const DevicePanel& v, DevicePanel q, ReduceLedger& ledger) {
   QrResult o{q, {v.cols, v.cols, std::vector<double>(v.cols * v.cols)}};
   bo_status st{};
-  check(bo_cholqr(c.get(), v.data, v.ld, v.cols, q.data, q.ld, o.r.a.data(), ledger.counts.data(), &st), st);
+  check(bo_cholqr(c.get(), v.data, v.ld, v.cols, q.data, q.ld, o.r.a.data(), LedgerIO(ledger).data(), &st), st);
   return o;
 }
 inline QrResult cholqr2(Context& c, const DevicePanel& v, DevicePanel q, ReduceLedger& ledger) {
   QrResult o{q, {v.cols, v.cols, std::vector<double>(v.cols * v.cols)}};
   bo_status st{};
-  check(bo_cholqr2(c.get(), v.data, v.ld, v.cols, q.data, q.ld, o.r.a.data(), ledger.counts.data(), &st), st);
+  check(bo_cholqr2(c.get(), v.data, v.ld, v.cols, q.data, q.ld, o.r.a.data(), LedgerIO(ledger).data(), &st), st);
   return o;
 }
 inline QrResult rand_cholqr(Context& c, const DevicePanel& v, const SketchOperator& theta, DevicePanel q,
                             ReduceLedger& ledger) {
   QrResult o{q, {v.cols, v.cols, std::vector<double>(v.cols * v.cols)}};
   bo_status st{};
-  check(bo_rand_cholqr(c.get(), v.data, v.ld, v.cols, theta.get(), q.data, q.ld, o.r.a.data(), ledger.counts.data(),
+  check(bo_rand_cholqr(c.get(), v.data, v.ld, v.cols, theta.get(), q.data, q.ld, o.r.a.data(), LedgerIO(ledger).data(),
                        &st),
         st);
   return o;
@@ -173,7 +259,10 @@ class BasisStore {
   uint64_t cols() const { return bo_basis_cols(h_); }
   ReduceLedger ledger() const {
     ReduceLedger l;
-    bo_basis_ledger(h_, l.counts.data());
+    uint64_t c[4];
+    bo_basis_ledger(h_, c);
+    for (int p = 0; p < 4; ++p)
+      for (uint64_t d = 0; d < c[p]; ++d) l.record((ReducePhase)p);
     return l;
   }
   DevicePanel basis() const {

@@ -208,6 +208,16 @@ int bo_basis_boundaries(bo_basis b, uint64_t* out);
 uint64_t bo_basis_sketched(bo_basis b, double* out, uint64_t* rows);
 /* local rows of basis columns [lo, hi) to host (n_local x (hi-lo)) */
 int bo_basis_cols_to_host(bo_basis b, uint64_t lo, uint64_t hi, double* out, bo_status* st);
+/* the arguments of the store's last push_panel (block_orth.cpp:76-98): base
+ * (= p), k, overlap, proj (base x k, ld base) and diag (k x k upper, ld k), so
+ * a host BasisStore can replay the push with the reference's own arithmetic */
+int bo_basis_last_push(bo_basis b, uint64_t* base, uint64_t* k, int* overlap, double* proj, double* diag);
+/* load a host BasisStore's state (first cols columns of Q, this rank's rows,
+ * ld ldq; R and C cols x cols column-major; seed flags; panel boundaries) so
+ * device calls continue from it (the reverse of bo_basis_last_push) */
+int bo_basis_import(bo_basis b, uint64_t cols, const double* q_host, uint64_t ldq, const double* r,
+                    const double* c, const unsigned char* seeded, const uint64_t* bounds, uint64_t nbounds,
+                    bo_status* st);
 
 /* bcgs_project_range (block_orth.hpp:111): vhat device, coeffs host (hi-lo) x k */
 int bo_bcgs_project_range(bo_basis b, const double* v, uint64_t ldv, uint64_t k, uint64_t lo,

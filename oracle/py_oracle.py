@@ -19,6 +19,8 @@ import numpy as np
 HERE = Path(__file__).resolve().parent
 ORC_LIB = HERE / "liboracle.so"
 REF_LIB = HERE / "_ref" / "libblkorth_ref.so"
+# the reference GMRES driver with its bcgs2 on the GPU (oracle/Makefile target refgpu)
+REFGPU_LIB = HERE / "_ref" / "libblkorth_refgpu.so"
 
 dp = C.POINTER(C.c_double)
 sz = C.c_size_t
@@ -86,7 +88,7 @@ class Oracle:
     def __init__(self, which: str = "orc"):
         self.which = which
         ensure_built(ref=(which == "ref"))
-        path = ORC_LIB if which == "orc" else REF_LIB
+        path = {"orc": ORC_LIB, "ref": REF_LIB, "refgpu": REFGPU_LIB}[which]
         if not path.exists():
             raise FileNotFoundError(path)
         self.lib = C.CDLL(str(path))

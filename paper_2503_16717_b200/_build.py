@@ -106,7 +106,8 @@ def build_oracle(verbose: bool = False) -> None:
         return
     subprocess.run(["make", "-s", "-C", str(odir), "all"], check=True)
     if Path("/root/reference/proj/src").exists():
-        subprocess.run(["make", "-s", "-C", str(odir), "ref"], check=True)
+        # the reference, and the reference driver on the GPU path (needs libbo_cuda.so)
+        subprocess.run(["make", "-s", "-C", str(odir), "ref"] + (["refgpu"] if LIB.exists() else []), check=True)
 
 
 if __name__ == "__main__":

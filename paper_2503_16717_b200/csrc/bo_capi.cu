@@ -1391,6 +1391,43 @@ extern "C" int bo_basis_cols_to_host(bo_basis b, uint64_t lo, uint64_t hi, doubl
   return BO_OK;
 }
 
+extern "C" int bo_basis_last_push(bo_basis b, uint64_t* base, uint64_t* k, int* overlap, double* proj,
+                                  double* diag) {
+  if (base) *base = b->last_base;
+  if (k) *k = b->last_k;
+  if (overlap) *overlap = b->last_overlap;
+  if (proj) std::copy(b->last_proj.begin(), b->last_proj.end(), proj);
+  if (diag) std::copy(b->last_diag.begin(), b->last_diag.end(), diag);
+  return BO_OK;
+}
+
+extern "C" int bo_basis_import(bo_basis b, uint64_t cols, const double* q_host, uint64_t ldq, const double* r,
+                               const double* c, const unsigned char* seeded, const uint64_t* bounds,
+                               uint64_t nbounds, bo_status* st) {
+  ok_st(st);
+  bo_ctx ctx = b->ctx;
+  if (cols > b->cap) return set_st(st, BO_INVALID, 0, 0.0, "import: %llu columns exceed the capacity %llu",
+                                   (unsigned long long)cols, (unsigned long long)b->cap);
+  if (cols > 0 && ldq < ctx->n_local) return set_st(st, BO_INVALID, 0, 0.0, "import: ldq < local rows");
+  CU(cudaStreamSynchronize(ctx->stream));
+  if (cols > 0)
+    CU(cudaMemcpy2D(b->q, ctx->ld * 8, q_host, ldq * 8, ctx->n_local * 8, cols, cudaMemcpyHostToDevice));
+  const uint64_t cap = b->cap;
+  std::fill(b->r.begin(), b->r.end(), 0.0);
+  std::fill(b->c.begin(), b->c.end(), 0.0);
+  std::fill(b->seeded.begin(), b->seeded.end(), 0);
+  for (uint64_t j = 0; j < cols; ++j) {
+    for (uint64_t i = 0; i < cols; ++i) {
+      b->r[i + j * cap] = r[i + j * cols];
+      if (c) b->c[i + j * cap] = c[i + j * cols];
+    }
+    b->seeded[j] = seeded ? seeded[j] : 0;
+  }
+  b->bounds.assign(bounds, bounds + nbounds);
+  b->cols = cols;
+  return BO_OK;
+}
+
 namespace bo {
 namespace host {
 // push_panel bookkeeping (block_orth.cpp:57-98) — Q columns are already in the slab
@@ -1399,6 +1436,15 @@ void push_panel_host(bo_basis b, uint64_t k, const double* proj, uint64_t ldp, c
                      bool overlap) {
   const uint64_t cap = b->cap;
   const uint64_t base = overlap ? b->cols - 1 : b->cols;
+  b->last_base = base;
+  b->last_k = k;
+  b->last_overlap = overlap ? 1 : 0;
+  b->last_proj.assign(base * k, 0.0);
+  b->last_diag.assign(k * k, 0.0);
+  for (uint64_t j = 0; j < k; ++j) {
+    for (uint64_t i = 0; i < base; ++i) b->last_proj[i + j * base] = proj[i + j * ldp];
+    for (uint64_t i = 0; i <= j; ++i) b->last_diag[i + j * k] = diag[i + j * ldd];
+  }
   if (overlap) {  // fold_overlap_column (block_orth.cpp:59-73)
     const uint64_t k0 = b->cols - 1;
     const double scale = diag[0];

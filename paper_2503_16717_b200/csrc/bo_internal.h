@@ -91,6 +91,11 @@ struct bo_basis_s {
   std::vector<double> sk;  // sketched history sk_rows x sk_cols
   uint64_t sk_rows = 0, sk_cols = 0;
   uint64_t ledger[4] = {0, 0, 0, 0};
+  // the arguments of the last push_panel (bo_basis_last_push: lets a host
+  // BasisStore replay the push with the reference's own arithmetic)
+  std::vector<double> last_proj, last_diag;
+  uint64_t last_base = 0, last_k = 0;
+  int last_overlap = 0;
 };
 
 struct bo_op_s {

@@ -64,7 +64,9 @@ def test_gaussian_sketch_ulps(gpu, mk, orc, ddm_host, n, shat, seed):
     rounded log / sin / cos (bo_ddmath.cuh), so it equals, bit for bit, the
     reference formula under a correctly rounded libm (host build of the same
     math).  Against glibc (the reference as run) only glibc's own misroundings
-    remain: measured 0.16 % of entries, <= 3 ulp (tests/test_ddmath.py)."""
+    remain (~0.14 % of entries): a 1-ulp misrounding of log, sin or cos passes
+    through sqrt and two products, so the entry moves by 1-4 ulp (measured
+    histogram over 2.5e7 entries: 24505 x 1, 9065 x 2, 331 x 3, rare 4)."""
     ctx = mk(n)
     th = gpu.SketchOperator.build(ctx, "gaussian", n, shat, seed).dense_stage()
     mhat = 2 * (shat + 1)
@@ -77,8 +79,9 @@ def test_gaussian_sketch_ulps(gpu, mk, orc, ddm_host, n, shat, seed):
     u = ulps(th, want)
     frac = float(np.mean(u > 0))
     print(f"gaussian n={n} mhat={mhat}: vs glibc {frac:.4%} of entries differ, ulp histogram {np.bincount(u.ravel()).tolist()}")
-    assert u.max() <= 3, u.max()
+    assert u.max() <= 5, u.max()
     assert frac < 0.003, frac
+    assert float(np.mean(u > 2)) < 1e-4
 
 
 @pytest.mark.parametrize("kind", ["count", "gaussian"])
