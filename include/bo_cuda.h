@@ -226,6 +226,20 @@ int bo_bcgs_project_range(bo_basis b, const double* v, uint64_t ldv, uint64_t k,
 /* bcgs2 (block_orth.hpp:123-124) — the north_star unit of work */
 int bo_bcgs2(bo_basis b, const double* v, uint64_t ldv, uint64_t k, int intra, bo_sketch theta,
              int overlap, bo_status* st);
+/* Deferred bcgs2: the same call enqueued on the context stream without a host
+ * wait (the panel must stay valid until it has run).  Enqueue several (and
+ * bo_basis_mark_seed between them), then bo_basis_sync: the calls run back to
+ * back on the device, and the host bookkeeping (push_panel, mark_seed, ledger)
+ * is replayed in program order up to the first failing call, whose error (the
+ * text bo_bcgs2 would have returned) comes back with *failed = its index
+ * among the enqueued calls.  Calls after a failure are no-ops on the device
+ * and are dropped, so the store ends exactly where the synchronous API would
+ * have thrown.  bo_basis_cols is the speculative count (all calls succeed);
+ * every other basis accessor completes the pending calls first (an error they
+ * meet is kept for the next bo_basis_sync). */
+int bo_bcgs2_enqueue(bo_basis b, const double* v, uint64_t ldv, uint64_t k, int intra, bo_sketch theta,
+                     int overlap, bo_status* st);
+int bo_basis_sync(bo_basis b, uint64_t* failed, bo_status* st);
 /* bcgs_pip (block_orth.hpp:130), rand_bcgs_preproc (:137) */
 int bo_bcgs_pip(bo_basis b, const double* v, uint64_t ldv, uint64_t k, int overlap,
                 bo_status* st);

@@ -120,6 +120,8 @@ _SIGS = {
     "bo_basis_boundaries": (C.c_int, [vp, u64p]),
     "bo_basis_sketched": (u64, [vp, dp, u64p]),
     "bo_basis_cols_to_host": (C.c_int, [vp, u64, u64, dp, SP]),
+    "bo_bcgs2_enqueue": (C.c_int, [vp, vp, u64, u64, C.c_int, vp, C.c_int, SP]),
+    "bo_basis_sync": (C.c_int, [vp, u64p, SP]),
     "bo_basis_last_push": (C.c_int, [vp, u64p, u64p, C.POINTER(C.c_int), dp, dp]),
     "bo_basis_import": (C.c_int, [vp, u64, dp, u64, dp, dp, C.POINTER(C.c_ubyte), u64p, u64, SP]),
     "bo_bcgs_project_range": (C.c_int, [vp, vp, u64, u64, u64, u64, vp, u64, dp, SP]),

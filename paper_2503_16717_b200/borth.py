@@ -539,6 +539,19 @@ class BasisStore:
     def reset(self):
         self.ctx.lib.bo_basis_reset(self.h)
 
+    def sync(self):
+        """complete the deferred bcgs2 calls (bo_basis_sync); raises the first
+        failure with .call = the index of the failing call"""
+        failed = C.c_uint64()
+        st = L.Status()
+        rc = self.ctx.lib.bo_basis_sync(self.h, C.byref(failed), C.byref(st))
+        if rc != 0:
+            try:
+                _raise(rc, st)
+            except Error as e:
+                e.call = int(failed.value)
+                raise
+
     def cols(self) -> int:
         return int(self.ctx.lib.bo_basis_cols(self.h))
 
@@ -646,9 +659,13 @@ def bcgs_project(store: BasisStore, v) -> ProjectResult:
     return bcgs_project_range(store, v, 0, store.cols())
 
 
-def bcgs2(store: BasisStore, v, intra=CHOLQR2, theta: SketchOperator | None = None, overlap: bool = False):
-    _call(store.ctx.lib.bo_bcgs2, store.h, _ptr(v), _ld_of(v), v.shape[0], intra,
-          theta.h if theta is not None else None, int(overlap))
+def bcgs2(store: BasisStore, v, intra=CHOLQR2, theta: SketchOperator | None = None, overlap: bool = False,
+          defer: bool = False):
+    """bcgs2 (block_orth.hpp:123).  defer=True enqueues the call without a
+    host wait (bo_bcgs2_enqueue): errors surface at store.sync(), which raises
+    the first failing call's exception with .call = its index."""
+    fn = store.ctx.lib.bo_bcgs2_enqueue if defer else store.ctx.lib.bo_bcgs2
+    _call(fn, store.h, _ptr(v), _ld_of(v), v.shape[0], intra, theta.h if theta is not None else None, int(overlap))
 
 
 def bcgs_pip(store: BasisStore, v, overlap: bool = False):

@@ -1311,12 +1311,17 @@ extern "C" int bo_basis_create(bo_ctx ctx, uint64_t capacity, bo_basis* out, bo_
 }
 extern "C" int bo_basis_destroy(bo_basis b) {
   if (!b) return BO_OK;
+  basis_drain(b);
+  if (b->snap) cudaFreeHost(b->snap);
+  if (b->snap_st) cudaFreeHost(b->snap_st);
   cudaStreamSynchronize(b->ctx->stream);
   cudaFree(b->q);
   delete b;
   return BO_OK;
 }
 extern "C" int bo_basis_reset(bo_basis b) {
+  basis_drain(b);
+  b->deferred_code = 0;
   b->cols = 0;
   std::fill(b->r.begin(), b->r.end(), 0.0);
   std::fill(b->c.begin(), b->c.end(), 0.0);
@@ -1335,34 +1340,52 @@ extern "C" double* bo_basis_q_device(bo_basis b, uint64_t* ld) {
   return b->q;
 }
 extern "C" int bo_basis_ledger(bo_basis b, uint64_t out[4]) {
+  basis_drain(b);
   std::memcpy(out, b->ledger, sizeof b->ledger);
   return BO_OK;
 }
 extern "C" int bo_basis_r_copy(bo_basis b, double* out) {  // block_orth.cpp:33-38
+  basis_drain(b);
   for (uint64_t j = 0; j < b->cols; ++j)
     for (uint64_t i = 0; i < b->cols; ++i) out[i + j * b->cols] = i <= j ? b->r[i + j * b->cap] : 0.0;
   return BO_OK;
 }
-extern "C" double bo_basis_r_entry(bo_basis b, uint64_t i, uint64_t j) { return b->r[i + j * b->cap]; }
+extern "C" double bo_basis_r_entry(bo_basis b, uint64_t i, uint64_t j) {
+  basis_drain(b);
+  return b->r[i + j * b->cap];
+}
 extern "C" int bo_basis_c_copy(bo_basis b, double* out) {
+  basis_drain(b);
   for (uint64_t j = 0; j < b->cols; ++j)
     for (uint64_t i = 0; i < b->cols; ++i) out[i + j * b->cols] = b->c[i + j * b->cap];
   return BO_OK;
 }
 extern "C" int bo_basis_mark_seed(bo_basis b, uint64_t col) {  // block_orth.cpp:40-45
   if (col >= b->cols) return BO_INVALID;
+  if (!b->pend.empty()) {  // after the enqueued calls, in program order (bo_basis_sync)
+    bo_basis_s::Pending op;
+    op.kind = 1;
+    op.col = col;
+    b->pend.push_back(op);
+    return BO_OK;
+  }
   for (uint64_t i = 0; i < b->cap; ++i) b->c[i + col * b->cap] = 0.0;
   b->c[col + col * b->cap] = 1.0;
   b->seeded[col] = 1;
   return BO_OK;
 }
-extern "C" int bo_basis_is_seed(bo_basis b, uint64_t col) { return col < b->cap && b->seeded[col]; }
+extern "C" int bo_basis_is_seed(bo_basis b, uint64_t col) {
+  basis_drain(b);
+  return col < b->cap && b->seeded[col];
+}
 extern "C" int bo_basis_input_coeff_col(bo_basis b, uint64_t k, uint64_t len, double* out) {  // :47-52
+  basis_drain(b);
   const std::vector<double>& src = bo_basis_is_seed(b, k) ? b->c : b->r;
   for (uint64_t i = 0; i < len; ++i) out[i] = src[i + k * b->cap];
   return BO_OK;
 }
 extern "C" int bo_basis_begin_big_panel(bo_basis b, uint64_t sketch_rows, int overlap) {  // :54-57
+  basis_drain(b);
   b->bp_lo = b->cols - ((overlap && b->cols > 0) ? 1 : 0);
   b->sk.clear();
   b->sk_rows = sketch_rows;
@@ -1370,18 +1393,24 @@ extern "C" int bo_basis_begin_big_panel(bo_basis b, uint64_t sketch_rows, int ov
   return BO_OK;
 }
 extern "C" uint64_t bo_basis_big_panel_lo(bo_basis b) { return b->bp_lo; }
-extern "C" uint64_t bo_basis_num_boundaries(bo_basis b) { return b->bounds.size(); }
+extern "C" uint64_t bo_basis_num_boundaries(bo_basis b) {
+  basis_drain(b);
+  return b->bounds.size();
+}
 extern "C" int bo_basis_boundaries(bo_basis b, uint64_t* out) {
+  basis_drain(b);
   for (size_t i = 0; i < b->bounds.size(); ++i) out[i] = b->bounds[i];
   return BO_OK;
 }
 extern "C" uint64_t bo_basis_sketched(bo_basis b, double* out, uint64_t* rows) {
+  basis_drain(b);
   if (rows) *rows = b->sk_rows;
   if (out && !b->sk.empty()) std::memcpy(out, b->sk.data(), b->sk.size() * 8);
   return b->sk_cols;
 }
 extern "C" int bo_basis_cols_to_host(bo_basis b, uint64_t lo, uint64_t hi, double* out, bo_status* st) {
   ok_st(st);
+  TRY(basis_drain(b));
   bo_ctx ctx = b->ctx;
   if (hi < lo || hi > b->cap) return set_st(st, BO_INVALID, 0, 0.0, "bad column range");
   CU(cudaStreamSynchronize(ctx->stream));
@@ -1393,6 +1422,7 @@ extern "C" int bo_basis_cols_to_host(bo_basis b, uint64_t lo, uint64_t hi, doubl
 
 extern "C" int bo_basis_last_push(bo_basis b, uint64_t* base, uint64_t* k, int* overlap, double* proj,
                                   double* diag) {
+  basis_drain(b);
   if (base) *base = b->last_base;
   if (k) *k = b->last_k;
   if (overlap) *overlap = b->last_overlap;
@@ -1405,6 +1435,7 @@ extern "C" int bo_basis_import(bo_basis b, uint64_t cols, const double* q_host, 
                                const double* c, const unsigned char* seeded, const uint64_t* bounds,
                                uint64_t nbounds, bo_status* st) {
   ok_st(st);
+  TRY(basis_drain(b));
   bo_ctx ctx = b->ctx;
   if (cols > b->cap) return set_st(st, BO_INVALID, 0, 0.0, "import: %llu columns exceed the capacity %llu",
                                    (unsigned long long)cols, (unsigned long long)b->cap);
@@ -1512,6 +1543,7 @@ int dev_project(bo_basis b, const double* v, uint64_t ldv, int K, uint64_t lo, u
 extern "C" int bo_bcgs_project_range(bo_basis b, const double* v, uint64_t ldv, uint64_t k, uint64_t lo, uint64_t hi,
                                      double* vhat, uint64_t ldvh, double* coeffs, bo_status* st) {
   ok_st(st);
+  TRY(basis_drain(b));
   bo_ctx ctx = b->ctx;
   CU(cudaSetDevice(ctx->device));
   if (lo > hi || hi > b->cols) return set_st(st, BO_INVALID, 0, 0.0, "bad projection range");
@@ -1538,8 +1570,53 @@ extern "C" int bo_bcgs_project_range(bo_basis b, const double* v, uint64_t ldv, 
   return BO_OK;
 }
 
-extern "C" int bo_bcgs2(bo_basis b, const double* v, uint64_t ldv, uint64_t k, int intra, bo_sketch theta,
-                        int overlap, bo_status* st) {
+namespace bo {
+namespace host {
+// pinned snapshot of one enqueued call: its status word and the tiny factors
+// its host bookkeeping needs (Rin for a first panel; coefficients and R_jj)
+int snapshot(bo_basis b, bo_basis_s::Pending& op, bo_status* st) {
+  bo_ctx ctx = b->ctx;
+  if (!b->snap) {
+    CU(cudaMallocHost((void**)&b->snap, (size_t)kSnapSlots * kSnapLen * 8));
+    CU(cudaMallocHost((void**)&b->snap_st, (size_t)kSnapSlots * sizeof(DevStatus)));
+  }
+  op.slot = b->nsnap++;
+  double* sn = b->snap + (size_t)op.slot * kSnapLen;
+  CU(cudaMemcpyAsync(&b->snap_st[op.slot], ctx->status, sizeof(DevStatus), cudaMemcpyDeviceToHost, ctx->stream));
+  if (op.first) {
+    CU(cudaMemcpyAsync(sn + kSnapRin, ctx->tiny + OFF_RIN, 256 * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  } else {
+    CU(cudaMemcpyAsync(sn + kSnapCoef, ctx->tiny + OFF_COEF, (size_t)LDC * 16 * 8, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CU(cudaMemcpyAsync(sn + kSnapRjj, ctx->tiny + OFF_RJJ, 256 * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  b->pend.push_back(op);
+  b->cols = op.cols_before - (op.overlap ? 1 : 0) + op.k;  // speculative: as if the call succeeds
+  return BO_OK;
+}
+
+int basis_drain(bo_basis b) {
+  if (b->pend.empty()) return BO_OK;
+  bo_status tmp;
+  uint64_t failed = 0;
+  const uint64_t before = b->deferred_code ? b->deferred_call : 0;
+  const int rc = bo_basis_sync(b, &failed, &tmp);
+  if (rc == BO_CUDA || rc == BO_NCCL) return rc;
+  if (rc != BO_OK && !b->deferred_code) {
+    b->deferred_code = rc;
+    b->deferred_st = tmp;
+    b->deferred_call = before + failed;
+  }
+  return BO_OK;
+}
+}  // namespace host
+}  // namespace bo
+
+// bcgs2 (block_orth.cpp:207-226), enqueued: the passes and a snapshot of the
+// call's status word and output factors go on the stream; the host bookkeeping
+// is replayed by bo_basis_sync.  No host wait.
+extern "C" int bo_bcgs2_enqueue(bo_basis b, const double* v, uint64_t ldv, uint64_t k, int intra, bo_sketch theta,
+                                int overlap, bo_status* st) {
   ok_st(st);
   bo_ctx ctx = b->ctx;
   CU(cudaSetDevice(ctx->device));
@@ -1554,20 +1631,22 @@ extern "C" int bo_bcgs2(bo_basis b, const double* v, uint64_t ldv, uint64_t k, i
     return set_st(st, BO_INVALID, 0, 0.0, "unknown intra kind");
   const double* vv;
   uint64_t lv;
+  if (b->pend.size() >= (size_t)kSnapSlots) TRY(basis_drain(b));  // bounded queue
   TRY(stage_input(ctx, v, ldv, k, 0, &vv, &lv, st));
   double* qout = b->q + base * ctx->ld;
-  TRY(reset_status(ctx, st));
+  if (b->pend.empty()) TRY(reset_status(ctx, st));  // sticky across a batch: later calls skip after a failure
   const bool rand = intra == BO_INTRA_RAND_CHOLQR;
+  bo_basis_s::Pending op;
+  op.kind = 0;
+  op.k = k;
+  op.cols_before = b->cols;
+  op.overlap = eff_overlap;
+  op.rand = rand;
 
   if (hi == 0) {  // first panel: intra only (block_orth.cpp:212-215)
     TRY(dev_intra(ctx, vv, lv, K, intra, theta, qout, ctx->ld, st));
-    TRY(fetch(ctx, true, st));
-    const DevStatus& d = *ctx->status_host;
-    const int upto = d.code ? d.pass : 2;
-    if (upto >= 1) b->ledger[rand ? BO_LEDGER_SKETCH : BO_LEDGER_GRAM]++;
-    if (upto >= 2) b->ledger[BO_LEDGER_GRAM]++;
-    TRY(dev_error(ctx, "cholqr", st));
-    push_panel_host(b, k, nullptr, 1, ctx->tiny_host + OFF_RIN, 16, eff_overlap);
+    op.first = true;
+    TRY(snapshot(b, op, st));
     return BO_OK;
   }
 
@@ -1671,19 +1750,91 @@ extern "C" int bo_bcgs2(bo_basis b, const double* v, uint64_t ldv, uint64_t k, i
   r6.ldo = ctx->ld;
   r6.pass_id = 6;
   TRY(run_pass(ctx, r6, st));
-
-  TRY(fetch(ctx, true, st));
-  const DevStatus& d = *ctx->status_host;
-  // ledger (block_orth.cpp:218-221): proj, intra(2), proj, gram
-  const int upto = d.code ? d.pass : 5;
-  if (upto >= 1) b->ledger[BO_LEDGER_PROJECTION]++;
-  if (upto >= 2) b->ledger[rand ? BO_LEDGER_SKETCH : BO_LEDGER_GRAM]++;
-  if (upto >= 3) b->ledger[BO_LEDGER_GRAM]++;
-  if (upto >= 4) b->ledger[BO_LEDGER_PROJECTION]++;
-  if (upto >= 5) b->ledger[BO_LEDGER_GRAM]++;
-  TRY(dev_error(ctx, "cholqr", st));
-  push_panel_host(b, k, ctx->tiny_host + OFF_COEF, LDC, ctx->tiny_host + OFF_RJJ, 16, eff_overlap);
+  TRY(snapshot(b, op, st));
   return BO_OK;
+}
+
+// Complete the store's enqueued calls in program order: ledger events,
+// push_panel bookkeeping and deferred mark_seeds, up to the first failing
+// call, whose error is returned (*failed = its index among the enqueued
+// calls).  Calls after it were no-ops on the device (sticky status) and are
+// dropped, so the store is left as the sequential API would leave it.
+extern "C" int bo_basis_sync(bo_basis b, uint64_t* failed, bo_status* st) {
+  ok_st(st);
+  if (failed) *failed = 0;
+  if (b->pend.empty()) {
+    const int code = b->deferred_code;
+    if (code) {
+      if (st) *st = b->deferred_st;
+      if (failed) *failed = b->deferred_call;
+      b->deferred_code = 0;
+    }
+    return code;
+  }
+  bo_ctx ctx = b->ctx;
+  CU(cudaStreamSynchronize(ctx->stream));
+  std::vector<bo_basis_s::Pending> ops;
+  ops.swap(b->pend);
+  b->nsnap = 0;
+  b->cols = ops.front().cols_before;
+  int rc = BO_OK;
+  uint64_t call = 0;
+  for (const bo_basis_s::Pending& op : ops) {
+    if (op.kind == 1) {  // deferred mark_seed (block_orth.cpp:40-45)
+      for (uint64_t i = 0; i < b->cap; ++i) b->c[i + op.col * b->cap] = 0.0;
+      b->c[op.col + op.col * b->cap] = 1.0;
+      b->seeded[op.col] = 1;
+      continue;
+    }
+    const DevStatus& d = b->snap_st[op.slot];
+    const double* sn = b->snap + (size_t)op.slot * kSnapLen;
+    // ledger: the reduce events the call reached (block_orth.cpp:212-221)
+    if (op.first) {
+      const int upto = d.code ? d.pass : 2;
+      if (upto >= 1) b->ledger[op.rand ? BO_LEDGER_SKETCH : BO_LEDGER_GRAM]++;
+      if (upto >= 2) b->ledger[BO_LEDGER_GRAM]++;
+    } else {
+      const int upto = d.code ? d.pass : 5;
+      if (upto >= 1) b->ledger[BO_LEDGER_PROJECTION]++;
+      if (upto >= 2) b->ledger[op.rand ? BO_LEDGER_SKETCH : BO_LEDGER_GRAM]++;
+      if (upto >= 3) b->ledger[BO_LEDGER_GRAM]++;
+      if (upto >= 4) b->ledger[BO_LEDGER_PROJECTION]++;
+      if (upto >= 5) b->ledger[BO_LEDGER_GRAM]++;
+    }
+    if (d.code != ST_OK) {
+      *ctx->status_host = d;
+      rc = dev_error(ctx, "cholqr", st);
+      if (failed) *failed = call;
+      break;
+    }
+    if (op.first)
+      push_panel_host(b, op.k, nullptr, 1, sn + kSnapRin, 16, op.overlap);
+    else
+      push_panel_host(b, op.k, sn + kSnapCoef, LDC, sn + kSnapRjj, 16, op.overlap);
+    ++call;
+  }
+  {
+    bo_status t2;
+    const int r2 = reset_status(ctx, &t2);
+    if (r2 != BO_OK) {
+      if (st) *st = t2;
+      return r2;
+    }
+  }
+  return rc;
+}
+
+// bcgs2 with the reference's synchronous contract: enqueue, then sync
+extern "C" int bo_bcgs2(bo_basis b, const double* v, uint64_t ldv, uint64_t k, int intra, bo_sketch theta,
+                        int overlap, bo_status* st) {
+  TRY(basis_drain(b));
+  const int rc = bo_bcgs2_enqueue(b, v, ldv, k, intra, theta, overlap, st);
+  if (rc != BO_OK) {
+    bo_status tmp;
+    bo_basis_sync(b, nullptr, &tmp);  // drop what was enqueued
+    return rc;
+  }
+  return bo_basis_sync(b, nullptr, st);
 }
 
 extern "C" int bo_mt64_jump_window(uint64_t seed, uint64_t J, uint64_t* out312) {

@@ -167,6 +167,18 @@ struct Gm {
   double* ydev = nullptr;  // least-squares solution y (device)
   int grid = 0;
   std::vector<double> hpart;
+  std::vector<cudaEvent_t> ev;  // phase timing of the deferred panel loop (device time)
+  ~Gm() {
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+  }
+  cudaEvent_t event(size_t i) {
+    while (ev.size() <= i) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ev.push_back(e);
+    }
+    return ev[i];
+  }
 };
 
 // global sum over ranks of per-CTA partials (fixed order) -> host
@@ -567,7 +579,66 @@ extern "C" int bo_sstep_gmres(bo_op op, const double* b, const double* x0, const
     CycleState cs;
     const uint64_t panels = cfg->m / cfg->s;
     const uint64_t ppb = twostage ? cfg->shat / cfg->s : panels;
-    for (uint64_t j = 0; j < panels && !cs.happy && !cs.aborted; ++j) {
+    if (!twostage) {
+      // One-stage schemes: the panels are enqueued back to back (matrix powers,
+      // then bo_bcgs2_enqueue) and the host syncs once per restart.  A breakdown
+      // at panel f leaves the store as it was after panel f - 1 (the calls after
+      // it were device no-ops); panel f's matrix powers are recomputed and it is
+      // recovered exactly as the call-by-call loop does (gmres.cpp:421-436),
+      // then the remaining panels are enqueued again.
+      const int intra = cfg->scheme == BO_BCGS2_CHOLQR2 ? BO_INTRA_CHOLQR2 : BO_INTRA_RAND_CHOLQR;
+      uint64_t j0 = 0;
+      while (j0 < panels && !cs.happy && !cs.aborted) {
+        size_t ne = 0;
+        for (uint64_t j = j0; j < panels; ++j) {
+          const double* seed_vec = q1;
+          if (j > 0) {
+            const uint64_t k0 = store->cols - 1;  // speculative count: the columns are on the stream
+            bo_basis_mark_seed(store, k0);       // replayed in order by bo_basis_sync
+            seed_vec = store->q + k0 * ld;
+          }
+          CU(cudaEventRecord(g.event(ne++), ctx->stream));
+          TRY(bo_mpk(op, seed_vec, cfg->s, panel, ld, st));
+          CU(cudaEventRecord(g.event(ne++), ctx->stream));
+          bo_status pst;
+          const int prc = bo_bcgs2_enqueue(store, panel, ld, K, intra, theta, j > 0, &pst);
+          CU(cudaEventRecord(g.event(ne++), ctx->stream));
+          if (prc != BO_OK) {  // argument / launch errors, not breakdowns
+            bo_status tmp;
+            bo_basis_sync(store, nullptr, &tmp);
+            if (st) *st = pst;
+            return prc;
+          }
+        }
+        uint64_t failed = 0;
+        bo_status pst;
+        const int prc = bo_basis_sync(store, &failed, &pst);
+        for (size_t e = 0; e + 2 < ne; e += 3) {
+          float a = 0.f, b2 = 0.f;
+          cudaEventElapsedTime(&a, g.ev[e], g.ev[e + 1]);
+          cudaEventElapsedTime(&b2, g.ev[e + 1], g.ev[e + 2]);
+          rep->t_mpk += a;
+          rep->t_orth += b2;
+        }
+        if (prc == BO_CUDA || prc == BO_NCCL || prc == BO_INVALID) {
+          if (st) *st = pst;
+          return prc;
+        }
+        if (prc == BO_OK) break;
+        const uint64_t f = j0 + failed;
+        t0 = std::chrono::steady_clock::now();
+        const double* seed_vec = q1;
+        if (f > 0) seed_vec = store->q + (store->cols - 1) * ld;  // seed mark replayed by the sync
+        TRY(bo_mpk(op, seed_vec, cfg->s, panel, ld, st));
+        CU(cudaStreamSynchronize(ctx->stream));
+        rep->t_mpk += ms_since(t0);
+        t0 = std::chrono::steady_clock::now();
+        TRY(recover_panel(g, store, panel, ld, (int)K, f > 0, pst.msg, cs, st));
+        rep->t_orth += ms_since(t0);
+        j0 = f + 1;
+      }
+    }
+    for (uint64_t j = 0; twostage && j < panels && !cs.happy && !cs.aborted; ++j) {
       t0 = std::chrono::steady_clock::now();
       const double* seed_vec = q1;
       if (j > 0) {

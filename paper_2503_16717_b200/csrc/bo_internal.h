@@ -96,6 +96,24 @@ struct bo_basis_s {
   std::vector<double> last_proj, last_diag;
   uint64_t last_base = 0, last_k = 0;
   int last_overlap = 0;
+  // Deferred mode (bo_bcgs2_enqueue / bo_basis_sync): the device runs the
+  // enqueued calls back to back; each call's status word and output factors
+  // are snapshotted into pinned slots, and the host-side bookkeeping
+  // (push_panel, mark_seed, ledger) is replayed in program order at sync.
+  // `cols` is speculative (the value after every pending call succeeds).
+  struct Pending {
+    int kind;  // 0: bcgs2 push, 1: mark_seed
+    uint64_t col = 0, k = 0, cols_before = 0;
+    bool overlap = false, first = false, rand = false;
+    int slot = -1;
+  };
+  std::vector<Pending> pend;
+  double* snap = nullptr;            // pinned [kSnapSlots][kSnapLen]
+  bo::DevStatus* snap_st = nullptr;  // pinned [kSnapSlots]
+  int nsnap = 0;
+  int deferred_code = 0;             // first failure drained by an accessor, reported by the next sync
+  bo_status deferred_st{};
+  uint64_t deferred_call = 0;
 };
 
 struct bo_op_s {
@@ -185,6 +203,8 @@ struct PassReq {
 // tiny workspace layout (doubles) — all K x K factors have ld 16
 // projection coefficient blocks (p x K) have ld LDC = 256 (p <= 255 basis columns)
 constexpr int LDC = 256;
+// deferred-call snapshots (bo_bcgs2_enqueue): Rin | R_jj | coefficients
+constexpr int kSnapSlots = 64, kSnapRin = 0, kSnapRjj = 256, kSnapCoef = 512, kSnapLen = 512 + LDC * 16;
 constexpr int OFF_R1 = 0, OFF_R2 = 256, OFF_R3 = 512, OFF_RIN = 768, OFF_RJJ = 1024,
               OFF_G = 1280, OFF_R4 = 1536, OFF_C1 = 2048, OFF_C2 = OFF_C1 + LDC * 16,
               OFF_COEF = OFF_C2 + LDC * 16, OFF_S = OFF_COEF + LDC * 16, TINY_LEN = OFF_S + 8192;
@@ -210,6 +230,8 @@ constexpr int kNcclUint64 = 5;   // ncclUint64
 constexpr int kNcclSum = 0;
 
 int set_st(bo_status* st, int code, long long index, double pivot, const char* fmt, ...);
+// complete any deferred calls of the store (keeps their first error for bo_basis_sync)
+int basis_drain(bo_basis b);
 // return BO_CUDA with the error text from a bo_status*-returning function
 #define CU(call)                                                                            \
   do {                                                                                      \

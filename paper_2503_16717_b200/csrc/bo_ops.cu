@@ -1180,6 +1180,7 @@ int two_stage_common(bo_basis b, const double* v, uint64_t ldv, uint64_t k, int 
 
 extern "C" int bo_bcgs_pip(bo_basis b, const double* v, uint64_t ldv, uint64_t k, int overlap, bo_status* st) {
   ok_st(st);
+  TRY(basis_drain(b));
   bo_ctx ctx = b->ctx;
   CU(cudaSetDevice(ctx->device));
   const double* vv;
@@ -1192,6 +1193,7 @@ extern "C" int bo_bcgs_pip(bo_basis b, const double* v, uint64_t ldv, uint64_t k
 extern "C" int bo_rand_bcgs_preproc(bo_basis b, const double* v, uint64_t ldv, uint64_t k, bo_sketch theta,
                                     int overlap, bo_status* st) {
   ok_st(st);
+  TRY(basis_drain(b));
   bo_ctx ctx = b->ctx;
   CU(cudaSetDevice(ctx->device));
   const double* vv;
@@ -1204,6 +1206,7 @@ extern "C" int bo_rand_bcgs_preproc(bo_basis b, const double* v, uint64_t ldv, u
 extern "C" int bo_two_stage_panel(bo_basis b, const double* v, uint64_t ldv, uint64_t k, int preproc,
                                   bo_sketch theta, int overlap, bo_status* st) {
   ok_st(st);
+  TRY(basis_drain(b));
   if (preproc == BO_PREPROC_RAND_BCGS && !theta)
     return set_st(st, BO_INVALID, 0, 0.0, "rand_bcgs preprocessing needs a sketch operator");
   return two_stage_common(b, v, ldv, k, preproc, theta, overlap, st);
@@ -1212,6 +1215,7 @@ extern "C" int bo_two_stage_panel(bo_basis b, const double* v, uint64_t ldv, uin
 extern "C" int bo_two_stage_finish(bo_basis b, int preproc, int reorthogonalize, int record, double* stats,
                                    bo_status* st) {
   ok_st(st);
+  TRY(basis_drain(b));
   bo_ctx ctx = b->ctx;
   CU(cudaSetDevice(ctx->device));
   const uint64_t bp = b->bp_lo, w = b->cols - bp;

@@ -21,7 +21,7 @@ a = ap.parse_args()
 k = a.s + 1
 ctx = P.Context(a.n, device=0)
 torch.cuda.set_stream(ctx.stream)
-panels = bench.make_panels(P, ctx, torch, a.n, k, 6, 1e2, 1e2, 7)
+panels = bench.make_panels(P, ctx, argparse.Namespace(s=a.s, panels=6, kappa=1e2))
 intra = P.borth.RAND_CHOLQR if a.intra == "rand_cholqr" else P.borth.CHOLQR2
 theta = P.SketchOperator.build(ctx, a.sketch, a.n, a.s, 1) if intra == P.borth.RAND_CHOLQR else None
 st = P.BasisStore(ctx, 6 * k)

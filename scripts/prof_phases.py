@@ -1,6 +1,7 @@
 """Per-phase cycle split of the pass kernels over the C2 sequence (diagnostic
 library built with -DBO_PHASE_PROF=1, loaded through BO_LIB).
     BO_LIB=.../libbo_cuda_phase.so python scripts/prof_phases.py"""
+import argparse
 import ctypes as C
 import sys
 from pathlib import Path
@@ -16,7 +17,7 @@ from paper_2503_16717_b200 import _lib  # noqa: E402
 n, k = 8_000_000, 11
 ctx = P.Context(n, device=0)
 torch.cuda.set_stream(ctx.stream)
-panels = bench.make_panels(P, ctx, torch, n, k, 6, 1e2, 1e2, 7)
+panels = bench.make_panels(P, ctx, argparse.Namespace(s=k - 1, panels=6, kappa=1e2))
 theta = P.SketchOperator.build(ctx, "gaussian", n, 10, 1)
 st = P.BasisStore(ctx, 6 * k)
 lib = ctx.lib
