@@ -78,10 +78,10 @@ __device__ __forceinline__ void gen_transform(const GenArgs& a, const uint64_t* 
     const double u2 = (double)(y1 >> 11) * 0x1.0p-53;
     // correctly rounded log / sin / cos (bo_ddmath.cuh): the only differences
     // from the reference left are glibc's own misroundings (~0.1 % of inputs)
-    const double rr = sqrt(tiny::mul(-2.0, ddm::log_rn(u1)));
+    const double rr = sqrt(tiny::mul(-2.0, ddm::log_cr(u1)));
     const double ang = tiny::mul(6.283185307179586476925286766559, u2);
     double sn, cs;
-    ddm::sincos_rn(ang, &sn, &cs);
+    ddm::sincos_cr(ang, &sn, &cs);
     const double v0 = tiny::mul(a.scale, tiny::mul(rr, cs));
     const double v1 = tiny::mul(a.scale, tiny::mul(rr, sn));
     uint64_t c1 = col, r1 = row + 1;

@@ -9,6 +9,23 @@
 
 extern "C" {
 double ddm_log(double x) { return bo::ddm::log_rn(x); }
+// fast path with its certainty flag, and the combined (what the device uses)
+void ddm_fast_n(const double* x, const double* a, double* lg, double* s, double* c, unsigned char* okl,
+                unsigned char* oks, long n) {
+  for (long i = 0; i < n; ++i) {
+    bool o1, o2;
+    lg[i] = bo::ddm::log_fast(x[i], &o1);
+    bo::ddm::sincos_fast(a[i], s + i, c + i, &o2);
+    okl[i] = o1;
+    oks[i] = o2;
+  }
+}
+void ddm_cr_n(const double* x, const double* a, double* lg, double* s, double* c, long n) {
+  for (long i = 0; i < n; ++i) {
+    lg[i] = bo::ddm::log_cr(x[i]);
+    bo::ddm::sincos_cr(a[i], s + i, c + i);
+  }
+}
 void ddm_sincos(double a, double* s, double* c) { bo::ddm::sincos_rn(a, s, c); }
 void ddm_log_n(const double* x, double* y, long n) {
   for (long i = 0; i < n; ++i) y[i] = bo::ddm::log_rn(x[i]);
@@ -39,8 +56,8 @@ void box_muller_n(uint64_t seed, long npairs, int which, double* out) {
       s = std::sin(a);
       c = std::cos(a);
     } else {
-      lg = bo::ddm::log_rn(u1);
-      bo::ddm::sincos_rn(a, &s, &c);
+      lg = bo::ddm::log_cr(u1);
+      bo::ddm::sincos_cr(a, &s, &c);
     }
     const double r = std::sqrt(-2.0 * lg);
     out[2 * t] = r * c;
@@ -57,9 +74,9 @@ void theta_cr(uint64_t rng_seed, long n, long mhat, double* out) {
   for (long q = 0; q < total; q += 2) {
     const double u1 = ((double)(g() >> 11) + 1.0) * 0x1.0p-53;
     const double u2 = (double)(g() >> 11) * 0x1.0p-53;
-    const double r = std::sqrt(-2.0 * bo::ddm::log_rn(u1));
+    const double r = std::sqrt(-2.0 * bo::ddm::log_cr(u1));
     double s, c;
-    bo::ddm::sincos_rn(6.283185307179586476925286766559 * u2, &s, &c);
+    bo::ddm::sincos_cr(6.283185307179586476925286766559 * u2, &s, &c);
     out[q] = scale * (r * c);
     if (q + 1 < total) out[q + 1] = scale * (r * s);
   }
