@@ -919,9 +919,11 @@ __global__ void __launch_bounds__(pass_threads(UPD), 1)
       part[e] = sum;
     }
     if (SK == SK_COUNT) {
-      for (int e = tid; e < mh * K; e += NW * 32) {
+      // every slot of the partial is written (the columns past K with zeros):
+      // the cross-CTA tree reads the whole block
+      for (int e = tid; e < mh * 16; e += NW * 32) {
         const int i = e % mh, j = e / mh;
-        part[a.off_s + i + j * a.ld_s] = cacc[e];
+        part[a.off_s + i + j * a.ld_s] = j < K ? cacc[i + j * mh] : 0.0;
       }
     }
   }
