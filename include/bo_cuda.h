@@ -281,6 +281,19 @@ int bo_csr_host_arrays(bo_csr_host h, int64_t* row_ptr, int64_t* col, double* va
 int bo_csr_host_destroy(bo_csr_host h);
 int bo_mm_write(const char* path, uint64_t nrows, uint64_t ncols, const int64_t* row_ptr, const int64_t* col,
                 const double* val, bo_status* st);
+/* Cost model (cost_model.hpp:9-39, cost_model.cpp:38-111): exact integer
+ * per-restart-cycle flops (both orthogonalization passes), latency (global
+ * reduces), volume and storage of the tabulated schemes.  shat is forced to
+ * 1 / s / m for standard / sstep and sketch_eq_s / sketch_eq_m; mhat <= 0
+ * selects 2(shat+1).  Errors: BO_INVALID with the reference's InvalidScheme
+ * text.  Host only. */
+enum { BO_COST_STANDARD = 0, BO_COST_SSTEP = 1, BO_COST_SKETCH_EQ_S = 2, BO_COST_SKETCH_BETWEEN = 3,
+       BO_COST_SKETCH_EQ_M = 4 };
+typedef struct {
+  int64_t flops_total, flops_second, latency, volume, storage;
+} bo_cost_result;
+int bo_cost_eval(int scheme, int64_t n, int64_t m, int64_t s, int64_t shat, int64_t mhat, bo_cost_result* out,
+                 bo_status* st);
 /* gen_glued (problems.cpp:21-61): the glued test matrix n x (num_panels *
  * panel_width), bit-identical to the reference for the same arguments (the
  * config-2 input).  n must be the context's global row count;

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "blkorth/block_orth.hpp"
+#include "blkorth/cost_model.hpp"
 #include "blkorth/dense.hpp"
 #include "blkorth/errors.hpp"
 #include "blkorth/gmres.hpp"
@@ -414,6 +415,30 @@ int ref_sstep_gmres(void* a, const double* b, const double* x0, const orc_solver
       rep->orth[i] = s.restart_orth_error[i];
       rep->arnoldi[i] = s.restart_arnoldi_resid[i];
     }
+  } catch (const Error& e) {
+    return fail(e);
+  }
+  return 0;
+}
+
+// cost_model.cpp:38-111 (eval_cost): out[5] = flops_total, flops_second,
+// latency, volume, storage; scheme 0..4 = standard, sstep, sketch_eq_s,
+// sketch_between, sketch_eq_m
+int ref_eval_cost(int scheme, int64_t n, int64_t m, int64_t s, int64_t shat, int64_t mhat, int64_t* out) {
+  try {
+    CostQuery q;
+    q.scheme = static_cast<CostScheme>(scheme);
+    q.n = n;
+    q.m = m;
+    q.s = s;
+    q.shat = shat;
+    q.mhat = mhat;
+    const CostResult r = eval_cost(q);
+    out[0] = r.flops_total;
+    out[1] = r.flops_second;
+    out[2] = r.latency;
+    out[3] = r.volume;
+    out[4] = r.storage;
   } catch (const Error& e) {
     return fail(e);
   }

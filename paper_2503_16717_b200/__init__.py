@@ -10,7 +10,7 @@ from .borth import (  # noqa: F401
     AllColumnsDiscarded, AmbientTooSmall, BasisStore, CholeskyBreakdown, Context, CudaError, Error,
     InvalidScheme, NcclError, Operator, ProjectResult, QrResult, RankDeficient, RecursiveQr, ReduceLedger,
     SingularTriangular, SketchOperator, ZeroMatrix, apply_inv_upper, bcgs2, bcgs_pip, bcgs_project,
-    bcgs_project_range, cholqr, cholqr2, gen_glued, gram, rand_bcgs_preproc, rand_cholqr, recursive_cholqr,
+    bcgs_project_range, cholqr, cholqr2, eval_cost, gen_glued, gram, rand_bcgs_preproc, rand_cholqr, recursive_cholqr,
     sstep_gmres_solve, two_stage_cycle, two_stage_finish, two_stage_panel,
 )
 

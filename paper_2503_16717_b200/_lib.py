@@ -132,6 +132,7 @@ _SIGS = {
     "bo_two_stage_finish": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, dp, SP]),
     "bo_op_csr": (C.c_int, [vp, u64, C.POINTER(i64), C.POINTER(i64), dp, C.POINTER(vp), SP]),
     "bo_op_laplace": (C.c_int, [vp, C.c_int, u64, C.POINTER(vp), SP]),
+    "bo_cost_eval": (C.c_int, [C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, SP]),
     "bo_gen_glued": (C.c_int, [vp, u64, u64, u64, C.c_double, C.c_double, u64, vp, u64, SP]),
     "bo_op_stencil": (C.c_int, [vp, C.c_int, u64, dp, C.POINTER(vp), SP]),
     "bo_op_destroy": (C.c_int, [vp]),

@@ -740,6 +740,21 @@ def gen_glued(ctx: Context, num_panels: int, panel_width: int, kappa_panel: floa
     return out
 
 
+COST_SCHEMES = {"standard": 0, "sstep": 1, "sketch_eq_s": 2, "sketch_between": 3, "sketch_eq_m": 4}
+
+
+def eval_cost(scheme, n: int, m: int, s: int = 1, shat: int = 1, mhat: int = 0) -> dict:
+    """eval_cost (cost_model.hpp:39): the per-restart-cycle cost-table entries
+    as exact integers; raises InvalidScheme with the reference's messages."""
+    if isinstance(scheme, str):
+        if scheme not in COST_SCHEMES:
+            raise InvalidScheme(f"unknown cost scheme '{scheme}'")
+        scheme = COST_SCHEMES[scheme]
+    out = (C.c_int64 * 5)()
+    _call(L.load().bo_cost_eval, scheme, n, m, s, shat, mhat, C.cast(out, C.c_void_p))
+    return dict(zip(("flops_total", "flops_second", "latency", "volume", "storage"), list(out)))
+
+
 # -------------------------------------------------------------- operator --
 def convdiff_coeffs(w: float = 0.3):
     """7-point coefficients (i-1, j-1, l-1, self, l+1, j+1, i+1) of the config-5

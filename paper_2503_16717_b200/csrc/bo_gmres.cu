@@ -58,6 +58,53 @@ __global__ void __launch_bounds__(256) sumsq_kernel(long long n, const double* _
   if (threadIdx.x == 0) part[blockIdx.x] = red[0];
 }
 
+// Standard GMRES (gmres.cpp:327-386), one column-wise projection step:
+// w -= (*dot_a) q_a (when q_a is given; unfused, as the reference's
+// w[t] -= dot * q(t, i)), then the per-CTA partial of q_b . w over the
+// updated w (q_b == w: the norm; q_b == nullptr: none).  Fixed-order block sum.
+__global__ void __launch_bounds__(256) cgs_update_dot_kernel(long long n, const double* __restrict__ qa,
+                                                             const double* __restrict__ dot_a, double* w,
+                                                             const double* qb, double* __restrict__ part) {
+  __shared__ double red[256];
+  const double d = qa ? *dot_a : 0.0;
+  double s = 0.0;
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
+    double wi = w[i];
+    if (qa) {
+      wi = __dsub_rn(wi, __dmul_rn(d, qa[i]));
+      w[i] = wi;
+    }
+    if (qb) s = fma(qb == w ? wi : qb[i], wi, s);
+  }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int k = 128; k > 0; k >>= 1) {
+    if (threadIdx.x < k) red[threadIdx.x] += red[threadIdx.x + k];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+// sum of the per-CTA partials in a fixed order -> *out; optionally h += sum
+__global__ void __launch_bounds__(256) finish_dot_kernel(int nparts, const double* __restrict__ part, double* out,
+                                                         double* h_entry) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += 256) s += part[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int k = 128; k > 0; k >>= 1) {
+    if (threadIdx.x < k) red[threadIdx.x] += red[threadIdx.x + k];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    *out = red[0];
+    if (h_entry) *h_entry += red[0];
+  }
+}
+
+__global__ void add_to_kernel(const double* src, double* dst) { *dst += *src; }
+
 // y = alpha * x
 __global__ void scale_kernel(long long n, double alpha, const double* __restrict__ x, double* __restrict__ y,
                              int divide) {
@@ -222,6 +269,88 @@ int true_residual(Gm& g, const double* b, const double* x, double* ax, double* r
   double s;
   TRY(reduce_sum(g, g.grid, &s, st));
   *gamma = std::sqrt(s);
+  return BO_OK;
+}
+
+double ms_since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// One restart cycle of standard GMRES (gmres.cpp:327-386): column-wise
+// Arnoldi with two projection passes per column (within a pass each q_i is
+// removed from the current w, in the reference's order), one projection reduce
+// per pass and one norm reduce per column in the ledger.  Basis columns land
+// in Q (ld), the Hessenberg entries in H ((m+1) x m, host).  A comparator
+// (SURVEY.md §8(f)4): every dot is its own reduction, so it is launch bound.
+int cgs2_cycle(Gm& g, double* Q, uint64_t ld, const double* q1, uint64_t m, double* w, double* dev, hd::Mat& H,
+               uint64_t& q_in, bool& happy, uint64_t led[4], double* t_mpk, double* t_orth, bo_status* st) {
+  bo_ctx ctx = g.ctx;
+  const long long nl = (long long)ctx->n_local;
+  double* hdev = dev;                 // (m + 1) x m Hessenberg, column-major
+  double* dots = dev + (m + 1) * m;   // m + 1 projection coefficients
+  double* nrm2 = dots + m + 1;        // 1
+  CU(cudaMemsetAsync(hdev, 0, (m + 1) * m * 8, ctx->stream));
+  CU(cudaMemcpyAsync(Q, q1, nl * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+  H = hd::Mat(m + 1, m);
+  q_in = m;
+  happy = false;
+  auto finish = [&](double* out, double* h_entry) -> int {
+    finish_dot_kernel<<<1, 256, 0, ctx->stream>>>(g.grid, g.part, out, ctx->world > 1 ? nullptr : h_entry);
+    CU(cudaGetLastError());
+    ctx->launches++;
+    if (ctx->world > 1) {
+      TRY(comm_allreduce(ctx, out, 1, st));
+      if (h_entry) {
+        add_to_kernel<<<1, 1, 0, ctx->stream>>>(out, h_entry);
+        CU(cudaGetLastError());
+        ctx->launches++;
+      }
+    }
+    return BO_OK;
+  };
+  auto upd = [&](const double* qa, const double* da, const double* qb) -> int {
+    cgs_update_dot_kernel<<<g.grid, 256, 0, ctx->stream>>>(nl, qa, da, w, qb, g.part);
+    CU(cudaGetLastError());
+    ctx->launches++;
+    return BO_OK;
+  };
+  std::vector<double> hk(m + 2);
+  for (uint64_t k = 0; k < m; ++k) {
+    auto t0 = std::chrono::steady_clock::now();
+    TRY(op_apply(g.op, Q + k * ld, w, st));
+    *t_mpk += ms_since(t0);
+    t0 = std::chrono::steady_clock::now();
+    TRY(upd(nullptr, nullptr, Q));  // q_0 . w
+    for (int pass = 0; pass < 2; ++pass) {
+      led[BO_LEDGER_PROJECTION]++;
+      for (uint64_t i = 0; i <= k; ++i) {
+        TRY(finish(dots + i, hdev + i + k * (m + 1)));
+        const double* next = i < k ? Q + (i + 1) * ld : (pass == 0 ? Q : w);
+        TRY(upd(Q + i * ld, dots + i, next));
+      }
+    }
+    TRY(finish(nrm2, nullptr));  // ||w||^2
+    led[BO_LEDGER_NORM]++;
+    CU(cudaMemcpyAsync(hk.data(), hdev + k * (m + 1), (k + 1) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(&hk[m + 1], nrm2, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    const double hnorm = std::sqrt(hk[m + 1]);
+    double hcol = 0.0;
+    for (uint64_t i = 0; i <= k; ++i) {
+      H(i, k) = hk[i];
+      hcol += hk[i] * hk[i];
+    }
+    *t_orth += ms_since(t0);
+    if (hnorm <= 1e-12 * std::sqrt(hcol + hnorm * hnorm)) {
+      q_in = k + 1;
+      happy = true;
+      break;
+    }
+    H(k + 1, k) = hnorm;
+    scale_kernel<<<g.grid, 256, 0, ctx->stream>>>(nl, hnorm, w, Q + (k + 1) * ld, 1);
+    CU(cudaGetLastError());
+    ctx->launches++;
+  }
   return BO_OK;
 }
 
@@ -447,9 +576,6 @@ int diagnostics(Gm& g, bo_basis b, const hd::Mat& H, size_t q_in, double a_fro, 
   return BO_OK;
 }
 
-double ms_since(std::chrono::steady_clock::time_point t0) {
-  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-}
 
 }  // namespace
 
@@ -462,8 +588,6 @@ extern "C" int bo_sstep_gmres(bo_op op, const double* b, const double* x0, const
   // validate_config (gmres.cpp:34-46)
   if (!(cfg->rel_tol > 0.0 && cfg->rel_tol < 1.0)) return set_st(st, BO_INVALID, 0, 0.0, "rel_tol must lie in (0, 1)");
   if (cfg->max_restarts == 0) return set_st(st, BO_INVALID, 0, 0.0, "max_restarts must be positive");
-  if (cfg->scheme == BO_STANDARD_CGS2)
-    return set_st(st, BO_INVALID, 0, 0.0, "standard_cgs2 (column-wise baseline) is not part of the GPU block path");
   if (cfg->s < 1 || cfg->s > cfg->shat || cfg->shat > cfg->m) return set_st(st, BO_INVALID, 0, 0.0, "need 1 <= s <= shat <= m");
   if (cfg->shat % cfg->s != 0) return set_st(st, BO_INVALID, 0, 0.0, "s must divide shat");
   if (cfg->m % cfg->shat != 0) return set_st(st, BO_INVALID, 0, 0.0, "shat must divide m");
@@ -475,7 +599,8 @@ extern "C" int bo_sstep_gmres(bo_op op, const double* b, const double* x0, const
   if ((cfg->scheme == BO_TWOSTAGE_PIP || cfg->scheme == BO_TWOSTAGE_RANDBCGS) && cfg->shat + 1 > 64)
     return set_st(st, BO_INVALID, 0, 0.0, "two-stage big panel shat + 1 > 64 columns is not supported by the GPU engine");
   if (cfg->n != 0 && cfg->n != ctx->n_global) return set_st(st, BO_INVALID, 0, 0.0, "config n does not match the matrix dimension");
-  if (cfg->s + 1 > 16) return set_st(st, BO_INVALID, 0, 0.0, "s > 15 is outside the streaming-pass engine");
+  const bool cgs2 = cfg->scheme == BO_STANDARD_CGS2;
+  if (!cgs2 && cfg->s + 1 > 16) return set_st(st, BO_INVALID, 0, 0.0, "s > 15 is outside the streaming-pass engine");
   const uint64_t n = ctx->n_global, nl = ctx->n_local, ld = ctx->ld;
   const uint64_t K = cfg->s + 1;
 
@@ -499,6 +624,13 @@ extern "C" int bo_sstep_gmres(bo_op op, const double* b, const double* x0, const
       for (void* q : p) cudaFree(q);
     }
   } fr{{g.part, g.gsum, g.ydev, r, ax, q1, panel}};
+  double *wbuf = nullptr, *cgsdev = nullptr;  // standard GMRES: w and the Hessenberg / dot scratch
+  if (cgs2) {
+    CU(cudaMalloc(&wbuf, ld * 8));
+    CU(cudaMalloc(&cgsdev, ((cfg->m + 1) * cfg->m + cfg->m + 2) * 8));
+    fr.p.push_back(wbuf);
+    fr.p.push_back(cgsdev);
+  }
 
   uint64_t extra[4] = {0, 0, 0, 0};
   // ||A||_F (gmres.cpp:286-288)
@@ -577,98 +709,128 @@ extern "C" int bo_sstep_gmres(bo_op op, const double* b, const double* x0, const
     ctx->launches++;
 
     CycleState cs;
-    const uint64_t panels = cfg->m / cfg->s;
-    const uint64_t ppb = twostage ? cfg->shat / cfg->s : panels;
-    if (!twostage) {
-      // One-stage schemes: the panels are enqueued back to back (matrix powers,
-      // then bo_bcgs2_enqueue) and the host syncs once per restart.  A breakdown
-      // at panel f leaves the store as it was after panel f - 1 (the calls after
-      // it were device no-ops); panel f's matrix powers are recomputed and it is
-      // recovered exactly as the call-by-call loop does (gmres.cpp:421-436),
-      // then the remaining panels are enqueued again.
-      const int intra = cfg->scheme == BO_BCGS2_CHOLQR2 ? BO_INTRA_CHOLQR2 : BO_INTRA_RAND_CHOLQR;
-      uint64_t j0 = 0;
-      while (j0 < panels && !cs.happy && !cs.aborted) {
-        size_t ne = 0;
-        for (uint64_t j = j0; j < panels; ++j) {
-          const double* seed_vec = q1;
-          if (j > 0) {
-            const uint64_t k0 = store->cols - 1;  // speculative count: the columns are on the stream
-            bo_basis_mark_seed(store, k0);       // replayed in order by bo_basis_sync
-            seed_vec = store->q + k0 * ld;
+    hd::Mat H;
+    uint64_t q_in = 0;
+    double t_h = 0.0;
+    if (cgs2) {  // standard GMRES comparator (gmres.cpp:327-386)
+      uint64_t led[4] = {0, 0, 0, 0};
+      TRY(cgs2_cycle(g, store->q, ld, q1, cfg->m, wbuf, cgsdev, H, q_in, cs.happy, led, &rep->t_mpk, &rep->t_orth,
+                     st));
+      acc_ledger(led);
+      const uint64_t p = cs.happy ? q_in : q_in + 1;
+      hd::Mat He(p, q_in);
+      for (uint64_t j = 0; j < q_in; ++j)
+        for (uint64_t i = 0; i < p; ++i) He(i, j) = H(i, j);
+      H = He;
+      store->cols = p;  // the diagnostics read Q[:, 0:p]
+      t0 = std::chrono::steady_clock::now();
+    } else {
+      const uint64_t panels = cfg->m / cfg->s;
+      const uint64_t ppb = twostage ? cfg->shat / cfg->s : panels;
+      if (!twostage) {
+        // One-stage schemes: the panels are enqueued back to back (matrix powers,
+        // then bo_bcgs2_enqueue) and the host syncs once per restart.  A breakdown
+        // at panel f leaves the store as it was after panel f - 1 (the calls after
+        // it were device no-ops); panel f's matrix powers are recomputed and it is
+        // recovered exactly as the call-by-call loop does (gmres.cpp:421-436),
+        // then the remaining panels are enqueued again.
+        const int intra = cfg->scheme == BO_BCGS2_CHOLQR2 ? BO_INTRA_CHOLQR2 : BO_INTRA_RAND_CHOLQR;
+        uint64_t j0 = 0;
+        while (j0 < panels && !cs.happy && !cs.aborted) {
+          size_t ne = 0;
+          for (uint64_t j = j0; j < panels; ++j) {
+            const double* seed_vec = q1;
+            if (j > 0) {
+              const uint64_t k0 = store->cols - 1;  // speculative count: the columns are on the stream
+              bo_basis_mark_seed(store, k0);       // replayed in order by bo_basis_sync
+              seed_vec = store->q + k0 * ld;
+            }
+            CU(cudaEventRecord(g.event(ne++), ctx->stream));
+            TRY(bo_mpk(op, seed_vec, cfg->s, panel, ld, st));
+            CU(cudaEventRecord(g.event(ne++), ctx->stream));
+            bo_status pst;
+            const int prc = bo_bcgs2_enqueue(store, panel, ld, K, intra, theta, j > 0, &pst);
+            CU(cudaEventRecord(g.event(ne++), ctx->stream));
+            if (prc != BO_OK) {  // argument / launch errors, not breakdowns
+              bo_status tmp;
+              bo_basis_sync(store, nullptr, &tmp);
+              if (st) *st = pst;
+              return prc;
+            }
           }
-          CU(cudaEventRecord(g.event(ne++), ctx->stream));
-          TRY(bo_mpk(op, seed_vec, cfg->s, panel, ld, st));
-          CU(cudaEventRecord(g.event(ne++), ctx->stream));
+          uint64_t failed = 0;
           bo_status pst;
-          const int prc = bo_bcgs2_enqueue(store, panel, ld, K, intra, theta, j > 0, &pst);
-          CU(cudaEventRecord(g.event(ne++), ctx->stream));
-          if (prc != BO_OK) {  // argument / launch errors, not breakdowns
-            bo_status tmp;
-            bo_basis_sync(store, nullptr, &tmp);
+          const int prc = bo_basis_sync(store, &failed, &pst);
+          for (size_t e = 0; e + 2 < ne; e += 3) {
+            float a = 0.f, b2 = 0.f;
+            cudaEventElapsedTime(&a, g.ev[e], g.ev[e + 1]);
+            cudaEventElapsedTime(&b2, g.ev[e + 1], g.ev[e + 2]);
+            rep->t_mpk += a;
+            rep->t_orth += b2;
+          }
+          if (prc == BO_CUDA || prc == BO_NCCL || prc == BO_INVALID) {
             if (st) *st = pst;
             return prc;
           }
+          if (prc == BO_OK) break;
+          const uint64_t f = j0 + failed;
+          t0 = std::chrono::steady_clock::now();
+          const double* seed_vec = q1;
+          if (f > 0) seed_vec = store->q + (store->cols - 1) * ld;  // seed mark replayed by the sync
+          TRY(bo_mpk(op, seed_vec, cfg->s, panel, ld, st));
+          CU(cudaStreamSynchronize(ctx->stream));
+          rep->t_mpk += ms_since(t0);
+          t0 = std::chrono::steady_clock::now();
+          TRY(recover_panel(g, store, panel, ld, (int)K, f > 0, pst.msg, cs, st));
+          rep->t_orth += ms_since(t0);
+          j0 = f + 1;
         }
-        uint64_t failed = 0;
+      }
+      for (uint64_t j = 0; twostage && j < panels && !cs.happy && !cs.aborted; ++j) {
+        t0 = std::chrono::steady_clock::now();
+        const double* seed_vec = q1;
+        if (j > 0) {
+          const uint64_t k0 = store->cols - 1;
+          bo_basis_mark_seed(store, k0);
+          seed_vec = store->q + k0 * ld;
+        }
+        TRY(bo_mpk(op, seed_vec, cfg->s, panel, ld, st));
+        rep->t_mpk += ms_since(t0);
+        const bool overlap = j > 0;
+        t0 = std::chrono::steady_clock::now();
+        if (twostage && j % ppb == 0) bo_basis_begin_big_panel(store, theta ? theta->mhat : 0, overlap);
         bo_status pst;
-        const int prc = bo_basis_sync(store, &failed, &pst);
-        for (size_t e = 0; e + 2 < ne; e += 3) {
-          float a = 0.f, b2 = 0.f;
-          cudaEventElapsedTime(&a, g.ev[e], g.ev[e + 1]);
-          cudaEventElapsedTime(&b2, g.ev[e + 1], g.ev[e + 2]);
-          rep->t_mpk += a;
-          rep->t_orth += b2;
-        }
-        if (prc == BO_CUDA || prc == BO_NCCL || prc == BO_INVALID) {
+        int prc = twostage ? bo_two_stage_panel(store, panel, ld, K, preproc, theta, overlap, &pst)
+                           : bo_bcgs2(store, panel, ld, K,
+                                      cfg->scheme == BO_BCGS2_CHOLQR2 ? BO_INTRA_CHOLQR2 : BO_INTRA_RAND_CHOLQR, theta,
+                                      overlap, &pst);
+        if (prc == BO_CUDA || prc == BO_NCCL || prc == BO_INVALID) {  // not a numerical breakdown
           if (st) *st = pst;
           return prc;
         }
-        if (prc == BO_OK) break;
-        const uint64_t f = j0 + failed;
-        t0 = std::chrono::steady_clock::now();
-        const double* seed_vec = q1;
-        if (f > 0) seed_vec = store->q + (store->cols - 1) * ld;  // seed mark replayed by the sync
-        TRY(bo_mpk(op, seed_vec, cfg->s, panel, ld, st));
-        CU(cudaStreamSynchronize(ctx->stream));
-        rep->t_mpk += ms_since(t0);
-        t0 = std::chrono::steady_clock::now();
-        TRY(recover_panel(g, store, panel, ld, (int)K, f > 0, pst.msg, cs, st));
-        rep->t_orth += ms_since(t0);
-        j0 = f + 1;
-      }
-    }
-    for (uint64_t j = 0; twostage && j < panels && !cs.happy && !cs.aborted; ++j) {
-      t0 = std::chrono::steady_clock::now();
-      const double* seed_vec = q1;
-      if (j > 0) {
-        const uint64_t k0 = store->cols - 1;
-        bo_basis_mark_seed(store, k0);
-        seed_vec = store->q + k0 * ld;
-      }
-      TRY(bo_mpk(op, seed_vec, cfg->s, panel, ld, st));
-      rep->t_mpk += ms_since(t0);
-      const bool overlap = j > 0;
-      t0 = std::chrono::steady_clock::now();
-      if (twostage && j % ppb == 0) bo_basis_begin_big_panel(store, theta ? theta->mhat : 0, overlap);
-      bo_status pst;
-      int prc = twostage ? bo_two_stage_panel(store, panel, ld, K, preproc, theta, overlap, &pst)
-                         : bo_bcgs2(store, panel, ld, K,
-                                    cfg->scheme == BO_BCGS2_CHOLQR2 ? BO_INTRA_CHOLQR2 : BO_INTRA_RAND_CHOLQR, theta,
-                                    overlap, &pst);
-      if (prc == BO_CUDA || prc == BO_NCCL || prc == BO_INVALID) {  // not a numerical breakdown
-        if (st) *st = pst;
-        return prc;
-      }
-      if (prc != BO_OK) {
-        if (!twostage || store->cols == 0) {
-          TRY(recover_panel(g, store, panel, ld, (int)K, overlap, pst.msg, cs, st));
-        } else {
-          cs.aborted = true;
-          cs.detail = pst.msg;
+        if (prc != BO_OK) {
+          if (!twostage || store->cols == 0) {
+            TRY(recover_panel(g, store, panel, ld, (int)K, overlap, pst.msg, cs, st));
+          } else {
+            cs.aborted = true;
+            cs.detail = pst.msg;
+          }
         }
+        if (twostage && !cs.happy && !cs.aborted && (j + 1) % ppb == 0) {
+          bo_status fst;
+          int frc = bo_two_stage_finish(store, preproc, cfg->reorthogonalize, 0, nullptr, &fst);
+          if (frc == BO_CUDA || frc == BO_NCCL || frc == BO_INVALID) {
+            if (st) *st = fst;
+            return frc;
+          }
+          if (frc != BO_OK) {
+            cs.aborted = true;
+            cs.detail = std::string("second stage: ") + fst.msg;
+          }
+        }
+        rep->t_orth += ms_since(t0);
       }
-      if (twostage && !cs.happy && !cs.aborted && (j + 1) % ppb == 0) {
+      if (twostage && cs.aborted && store->cols > store->bp_lo && store->cols > 0) {
         bo_status fst;
         int frc = bo_two_stage_finish(store, preproc, cfg->reorthogonalize, 0, nullptr, &fst);
         if (frc == BO_CUDA || frc == BO_NCCL || frc == BO_INVALID) {
@@ -676,39 +838,25 @@ extern "C" int bo_sstep_gmres(bo_op op, const double* b, const double* x0, const
           return frc;
         }
         if (frc != BO_OK) {
-          cs.aborted = true;
-          cs.detail = std::string("second stage: ") + fst.msg;
+          cs.detail += "; basis after the last completed big panel unusable";
+          bo_basis_reset(store);  // BasisStore(n, 1): nothing to solve over, ledger dropped
         }
       }
-      rep->t_orth += ms_since(t0);
-    }
-    if (twostage && cs.aborted && store->cols > store->bp_lo && store->cols > 0) {
-      bo_status fst;
-      int frc = bo_two_stage_finish(store, preproc, cfg->reorthogonalize, 0, nullptr, &fst);
-      if (frc == BO_CUDA || frc == BO_NCCL || frc == BO_INVALID) {
-        if (st) *st = fst;
-        return frc;
-      }
-      if (frc != BO_OK) {
-        cs.detail += "; basis after the last completed big panel unusable";
-        bo_basis_reset(store);  // BasisStore(n, 1): nothing to solve over, ledger dropped
-      }
-    }
-    acc_ledger(store->ledger);
+      acc_ledger(store->ledger);
 
-    const uint64_t p = store->cols;
-    const uint64_t q_in = cs.happy ? p : (p > 0 ? p - 1 : 0);
-    if (q_in == 0) {
-      rep->breakdown = cs.aborted;
-      snprintf(rep->breakdown_detail, sizeof rep->breakdown_detail, "%s", cs.detail.c_str());
-      rep->final_relres = gamma / gamma0;
-      done = true;
-      continue;
+      const uint64_t p = store->cols;
+      q_in = cs.happy ? p : (p > 0 ? p - 1 : 0);
+      if (q_in == 0) {
+        rep->breakdown = cs.aborted;
+        snprintf(rep->breakdown_detail, sizeof rep->breakdown_detail, "%s", cs.detail.c_str());
+        rep->final_relres = gamma / gamma0;
+        done = true;
+        continue;
+      }
+      t0 = std::chrono::steady_clock::now();
+      TRY(assemble_hessenberg(store, q_in, cs.happy ? &cs.happy_col : nullptr, H, st));
+      t_h = ms_since(t0);
     }
-    t0 = std::chrono::steady_clock::now();
-    hd::Mat H;
-    TRY(assemble_hessenberg(store, q_in, cs.happy ? &cs.happy_col : nullptr, H, st));
-    const double t_h = ms_since(t0);
     std::vector<double> y;
     const double lsq = solve_lsq(H, gamma, y);
     const double t_l = ms_since(t0);

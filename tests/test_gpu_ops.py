@@ -218,7 +218,7 @@ def _gmres(gpu, mk, orc, k2d, **kw):
     op = gpu.Operator.laplace(ctx, 2, k2d)
     b = np.ones(n)
     x, rep = gpu.sstep_gmres_solve(op, ctx.from_host(b), ctx.from_host(np.zeros(n)), **kw)
-    scheme = {"bcgs2_cholqr2": 0, "bcgs2_randcholqr": 1, "twostage_pip": 2, "twostage_randbcgs": 3}[kw["scheme"]]
+    scheme = {"bcgs2_cholqr2": 0, "bcgs2_randcholqr": 1, "twostage_pip": 2, "twostage_randbcgs": 3, "standard_cgs2": 4}[kw["scheme"]]
     want = orc.sstep_gmres(csr, b, np.zeros(n), m=kw.get("m", 60), s=kw["s"], shat=kw.get("shat", 60),
                            scheme=scheme, sketch=kw.get("sketch_id", 0))
     return ctx, x, rep, want
@@ -375,3 +375,24 @@ def test_gmres_c1_from_matrix_market(gpu, mk, orc, tmp_path):
     assert rep["reduce"] == want["reduce"]
     for i, (g, w) in enumerate(zip(rep["restart_relres"], want["relres"])):
         assert abs(g - w) <= _envelope(i) * abs(w), (i, g, w)
+
+
+# standard GMRES comparator (gmres.cpp:327-386); the reference's
+# own sensitivity on config 1 (50 entries of b moved by one ulp, worst of 4):
+# 1.9e-14 9.9e-14 5.9e-13 5.9e-13 1.6e-11 3.6e-11 7.9e-9 4.6e-7 5.5e-4 1.0e-3
+CGS2_ENV = [1.9e-14, 9.9e-14, 5.9e-13, 5.9e-13, 1.6e-11, 3.6e-11, 7.9e-9, 4.6e-7, 5.5e-4, 1.0e-3]
+
+
+def test_gmres_standard_cgs2_c1(gpu, mk, orc):
+    """same 10 restarts / 600 iterations and ledger (1200 projection + 611
+    norm reduces) as the reference; relres within 10x its sensitivity,
+    floored at 1e-10; per-restart diagnostics of the same magnitude"""
+    ctx, x, rep, want = _gmres(gpu, mk, orc, 100, s=5, scheme="standard_cgs2")
+    assert rep["converged"] and want.converged
+    assert rep["restarts"] == want.restarts == 10 and rep["iterations"] == want.iterations == 600
+    assert rep["reduce"] == want.reduce == [1200, 0, 0, 611]
+    d = [abs(g - w) / w for g, w in zip(rep["restart_relres"], want.relres)]
+    print("cgs2 relres deltas", " ".join("%.1e" % v for v in d))
+    assert all(v <= max(1e-10, 10 * CGS2_ENV[i]) for i, v in enumerate(d))
+    assert max(rep["restart_orth_error"]) < 1e-12
+    assert all(0.5 <= g / w <= 2.0 for g, w in zip(rep["restart_arnoldi_resid"], want.arnoldi))

@@ -203,3 +203,33 @@ def test_matrix_market_write_matches_reference(ref, orc, tmp_path):
     assert (tmp_path / "ours.mtx").read_bytes() == (tmp_path / "ref.mtx").read_bytes()
     got = P.borth.read_matrix_market(tmp_path / "ours.mtx")
     assert np.array_equal(got[2], rp) and np.array_equal(got[3], ci) and np.array_equal(got[4], vv)
+
+
+def test_cost_model_matches_reference(ref):
+    """(f)4: bo_cost_eval restates cost_model.cpp:38-111 exactly (integers and
+    InvalidScheme texts), checked against the compiled reference's eval_cost"""
+    import ctypes as C
+    import paper_2503_16717_b200 as P
+    f = ref.lib.ref_eval_cost
+    f.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.POINTER(C.c_int64)]
+    f.restype = C.c_int
+    names = ["standard", "sstep", "sketch_eq_s", "sketch_between", "sketch_eq_m"]
+    checked = 0
+    for sc, name in enumerate(names):
+        for n in (1, 7, 10_000, 8_000_000, 64_000_000):
+            for m in (1, 7, 12, 60, 120):
+                for s in (1, 2, 3, 5, 10, 12, 15):
+                    for shat in (1, 4, 12, 30, 60):
+                        for mhat in (0, 22, 45):
+                            out = (C.c_int64 * 5)()
+                            rc = f(sc, n, m, s, shat, mhat, out)
+                            try:
+                                got = P.eval_cost(name, n, m, s, shat, mhat)
+                                assert rc == 0, (name, n, m, s, shat, mhat)
+                                assert list(got.values()) == list(out), (name, n, m, s, shat, mhat)
+                            except P.InvalidScheme as e:
+                                assert rc != 0, (name, n, m, s, shat, mhat)
+                                assert str(e) == ref.status()[1], (str(e), ref.status())
+                            checked += 1
+    assert checked > 10000
+    assert P.eval_cost("sstep", 8_000_000, 60, 10)["latency"] == 24
