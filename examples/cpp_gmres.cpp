@@ -26,6 +26,9 @@ int main(int argc, char** argv) {
     std::vector<double> ones(n, 1.0);
     cudaMemcpy(b, ones.data(), n * 8, cudaMemcpyHostToDevice);
     cudaMemset(x0, 0, n * 8);
+    // the pageable upload may still be in flight, and the context's private
+    // non-blocking stream does not wait for the legacy stream
+    cudaDeviceSynchronize();
     bo_solver_config cfg{};
     cfg.n = n;
     cfg.m = 60;

@@ -38,6 +38,7 @@ namespace {
 
 struct Mirror {
   bo_ctx ctx = nullptr;
+  cudaStream_t stream = nullptr;  // the context's stream: uploads are ordered before its passes
   uint64_t n = 0, ld = 0;
   bo_basis b = nullptr;
   uint64_t cap = 0;
@@ -64,9 +65,14 @@ void ensure_ctx(uint64_t n) {
   if (g.panel) cudaFree(g.panel);
   if (g.theta_dev) cudaFree(g.theta_dev);
   if (g.ctx) bo_ctx_destroy(g.ctx);
+  if (g.stream) cudaStreamDestroy(g.stream);
   g = Mirror{};
   bo_status st{};
-  ok(bo_ctx_create(0, 0, 1, nullptr, n, 0, n, nullptr, &g.ctx, &st), st);
+  // A pageable cudaMemcpy may return before its DMA lands, and a non-blocking
+  // library stream is not ordered after the legacy stream: every upload goes
+  // on the context's own stream instead.
+  cuda_ok(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
+  ok(bo_ctx_create(0, 0, 1, nullptr, n, 0, n, g.stream, &g.ctx, &st), st);
   g.n = n;
   g.ld = bo_ctx_ld(g.ctx);
   cuda_ok(cudaMalloc((void**)&g.panel, g.ld * 16 * sizeof(double)));
@@ -120,7 +126,7 @@ bo_sketch device_sketch(const SketchOperator* theta) {
     cuda_ok(cudaMalloc((void**)&g.theta_dev, g.ld * mh * sizeof(double)));
     g.theta_cols = mh;
   }
-  cuda_ok(cudaMemcpy2D(g.theta_dev, g.ld * 8, d.data(), g.n * 8, g.n * 8, mh, cudaMemcpyHostToDevice));
+  cuda_ok(cudaMemcpy2DAsync(g.theta_dev, g.ld * 8, d.data(), g.n * 8, g.n * 8, mh, cudaMemcpyHostToDevice, g.stream));
   bo_status st{};
   ok(bo_sketch_from_dense(g.ctx, g.theta_dev, g.ld, mh, &g.sk, &st), st);
   g.sk_key = d.data();
@@ -137,7 +143,7 @@ void gpu_bcgs2(BasisStore& store, const DenseMatrix& v, IntraKind intra, const S
   ensure_ctx(n);
   sync_store(store);
   bo_sketch sk = device_sketch(theta);
-  cuda_ok(cudaMemcpy2D(g.panel, g.ld * 8, v.data(), n * 8, n * 8, k, cudaMemcpyHostToDevice));
+  cuda_ok(cudaMemcpy2DAsync(g.panel, g.ld * 8, v.data(), n * 8, n * 8, k, cudaMemcpyHostToDevice, g.stream));
   uint64_t led0[4], led1[4];
   bo_basis_ledger(g.b, led0);
   bo_status st{};

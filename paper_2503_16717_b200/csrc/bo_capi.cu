@@ -210,6 +210,7 @@ int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st) {
   if (a.part_len == 0) a.part_len = 1;
 
   const int nt = r.K <= 8 ? 1 : 2;
+  const bool pre_qtx = ki.npre > 0 && ki.qtx, pre_upd = ki.npre > 0 && ki.upd;  // bo_pass.cuh consumer counts
   const size_t avail = std::min<size_t>(ctx->smem_optin, 227 * 1024) - 1024;  // static smem headroom
   // Tile choice: the largest tile (256 / 128 / 64 rows) whose stage ring is
   // at least double-buffered.  Per-tile synchronisation costs ~0.3-1 us
@@ -258,7 +259,7 @@ int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st) {
       const bool rft = !r.exact && (ki.npre > 0 || ki.npost > 0) && (r.K == 6 || r.K == 11 || r.K == 13 || r.K == 16);
       const size_t fixed = (xt ? 2 * (size_t)nt * 8 * S * 8 * nsub : 0) + (3 * 256 + 48 + (rft ? 3 * 256 : 0)) * 8 +
                            (ki.sk == SK_COUNT ? (size_t)mh * r.K * 8 : 0) + 3 * kMaxStages * 8;
-      const size_t need_red = (size_t)consumer_warps(ki.upd) * dm_len * 8;
+      const size_t need_red = (size_t)consumer_warps(ki.upd, pre_qtx, pre_upd) * dm_len * 8;
       const size_t need_fin = (1536 + (size_t)std::max(mh, 32) * 16 + 64) * 8;  // finalize_dev scratch
       if (avail <= fixed) continue;
       int ns = (int)std::min<size_t>(kMaxStages, (avail - fixed) / stage);
@@ -361,7 +362,7 @@ int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st) {
     TRY(make_tmap(&tmT, ki.sk == SK_GAUSS ? r.sk->theta : nullptr, ctx->n_local, mh,
                   ki.sk == SK_GAUSS ? r.sk->ldth : 0, S, st));
   }
-  fn<<<grid, pass_threads(ki.upd), total, ctx->stream>>>(a, tmV, tmQ, tmT);
+  fn<<<grid, pass_threads(ki.upd, pre_qtx, pre_upd), total, ctx->stream>>>(a, tmV, tmQ, tmT);
   CU(cudaGetLastError());
   ctx->launches++;
   if (ctx->profiling) {
@@ -1440,9 +1441,13 @@ extern "C" int bo_basis_import(bo_basis b, uint64_t cols, const double* q_host, 
   if (cols > b->cap) return set_st(st, BO_INVALID, 0, 0.0, "import: %llu columns exceed the capacity %llu",
                                    (unsigned long long)cols, (unsigned long long)b->cap);
   if (cols > 0 && ldq < ctx->n_local) return set_st(st, BO_INVALID, 0, 0.0, "import: ldq < local rows");
-  CU(cudaStreamSynchronize(ctx->stream));
+  // on the ctx stream: a pageable cudaMemcpy on the legacy stream may return
+  // before its DMA lands, and the non-blocking ctx stream would not wait for it
+  // (the reference driver's every-restart import raced its first pass)
   if (cols > 0)
-    CU(cudaMemcpy2D(b->q, ctx->ld * 8, q_host, ldq * 8, ctx->n_local * 8, cols, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy2DAsync(b->q, ctx->ld * 8, q_host, ldq * 8, ctx->n_local * 8, cols, cudaMemcpyHostToDevice,
+                         ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
   const uint64_t cap = b->cap;
   std::fill(b->r.begin(), b->r.end(), 0.0);
   std::fill(b->c.begin(), b->c.end(), 0.0);

@@ -26,10 +26,30 @@ constexpr int kMaxPTile = 64;    // max projection columns per streaming pass
 // 16 eight-row groups of a tile split evenly; 168 registers).  The
 // producer-less variant (BO_PRODUCER_WARP=0: the last warp to release a stage
 // issues its refill) measured 4% slower over the C2 sequence.
-__host__ __device__ constexpr int consumer_warps(bool upd) { return upd ? BO_NW_UPD : BO_NW_OTHER; }
-__host__ __device__ constexpr int pass_threads(bool upd) { return (consumer_warps(upd) + BO_PRODUCER_WARP) * 32; }
-constexpr int kMaxConsumerWarps = BO_NW_UPD > BO_NW_OTHER ? BO_NW_UPD : BO_NW_OTHER;
-constexpr int kMaxStages = 24;   // shared-memory stage ring depth bound
+// Pre-solve passes (two row-solve warps + a U/S/R group): the consumer count
+// of the projection (P2_QTX) and update (P2_UPD_*) kinds.  The update kinds
+// use 2 + 8: two U/S/R warps on every SM sub-partition (11 warps, 186
+// registers; they need 132).  Measured on the C2 sequence (scripts/ab_passes.sh):
+// P2_UPD_GRAM_ST 3.92 -> 3.68 ms; 2 + 6 leaves two sub-partitions with one
+// U/S/R warp and a solve warp, 4 + 8 starves the update of registers, and
+// P2_QTX is best at 2 + 5 (2 + 4 wins only at p >= 44, 4 + 4 and 3 + 4 lose).
+#ifndef BO_NW_PRE_QTX
+#define BO_NW_PRE_QTX BO_NW_OTHER
+#endif
+#ifndef BO_NW_PRE_UPD
+#define BO_NW_PRE_UPD 10
+#endif
+__host__ __device__ constexpr int consumer_warps(bool upd, bool pre_qtx = false, bool pre_upd = false) {
+  return pre_qtx ? BO_NW_PRE_QTX : pre_upd ? BO_NW_PRE_UPD : upd ? BO_NW_UPD : BO_NW_OTHER;
+}
+__host__ __device__ constexpr int pass_threads(bool upd, bool pre_qtx = false, bool pre_upd = false) {
+  return (consumer_warps(upd, pre_qtx, pre_upd) + BO_PRODUCER_WARP) * 32;
+}
+constexpr int kMaxStages = 24;
+// warps per CTA of the tile-per-warp engine (bo_tpw.cuh): one per SM sub-partition
+#ifndef BO_TPW_NW
+#define BO_TPW_NW 4
+#endif   // shared-memory stage ring depth bound
 
 // Tile geometry.  A tile of T rows is staged as T / R sub-tiles of R <= 128
 // rows; within a sub-tile an operand block is column-major with the padded

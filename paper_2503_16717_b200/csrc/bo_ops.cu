@@ -254,6 +254,152 @@ __global__ void __launch_bounds__(256, BO_SPMV_MINB) spmv_stencil4_halo_kernel(i
   }
 }
 
+// Plane-marching 3-D 7-point stencil (2.5-D blocking).  A CTA owns JB grid
+// lines j0 .. j0+JB-1 (all k points of each: k/PT threads per line, thread tx
+// of a line holds points l = tx + (k/PT) t, t < PT, so a warp's shared-memory
+// reads are consecutive doubles) and walks a range of planes i.  The lines
+// j0-1 .. j0+JB of one plane are contiguous in x, so each plane arrives with
+// ONE bulk async copy (TMA engine) into a 4-deep shared-memory ring tracked
+// by mbarriers, three planes ahead of the one being computed.  Every x value
+// is read from HBM once (plus the two halo lines per CTA, L2 hits); the i-1 /
+// i / i+1 values move through registers and the j-1 / j+1 / l-1 / l+1
+// neighbours come from the staged plane.  The previous kernel read each x
+// value seven times through L1/L2 and was bound there (38 us per SpMV at
+// n = 8e6).  Sums are formed exactly as in spmv_stencil_kernel (reference
+// order, unfused mul/add): bit-identical.
+// Planes: local plane q in [0, np) at x + q k^2; the plane below the shard
+// (q = -1) at hlo and the one above (q = np) at hhi (sharded halos).
+constexpr int kMarchRing = 4;
+template <int PT>
+__global__ void __launch_bounds__(512) spmv_stencil7_march_kernel(uint32_t k, uint32_t jb, uint32_t ip0, uint32_t np,
+                                                                  const Stencil st, const double* __restrict__ x,
+                                                                  const double* __restrict__ hlo,
+                                                                  const double* __restrict__ hhi,
+                                                                  double* __restrict__ y) {
+  extern __shared__ __align__(128) double plb[];  // [kMarchRing][(jb + 2) * k]: lines j0-1 .. j0+jb
+  __shared__ __align__(8) uint64_t full[kMarchRing];
+  const uint32_t G = k / PT, kk = k * k, pl = (jb + 2) * k;
+  const uint32_t tx = threadIdx.x % G, ty = threadIdx.x / G;
+  const uint32_t nbj = (k + jb - 1) / jb;
+  // the (line block, plane) steps are split into equal contiguous ranges, one
+  // per CTA (a persistent grid): every SM gets the same work; a range that
+  // crosses into the next line block restarts the march there
+  const uint64_t total = (uint64_t)nbj * np;
+  const uint64_t u0 = total * blockIdx.x / gridDim.x, u1 = total * (blockIdx.x + 1) / gridDim.x;
+  auto plane = [&](int q) -> const double* { return q < 0 ? hlo : (q >= (int)np ? hhi : x + (size_t)q * kk); };
+  // plane q (local) exists if its global index is in [0, k) and q in [-1, np]
+  auto exists = [&](int q) { return (int)ip0 + q >= 0 && (int)ip0 + q < (int)k && q >= -1 && q <= (int)np; };
+  auto buf = [&](int q) { return plb + (size_t)((q + kMarchRing) % kMarchRing) * pl; };
+  // pbits bit b = parity of the number of loads issued into buffer b (every
+  // thread tracks it); waiting for the latest load into b uses the opposite
+  uint32_t pbits = 0;
+  auto wait = [&](int q) {
+    const int b = (q + kMarchRing) % kMarchRing;
+    ptx::mbar_wait(&full[b], ((pbits >> b) & 1u) ^ 1u);
+  };
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < kMarchRing; ++b) ptx::mbar_init(&full[b], 1);
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+  const double c_ilo = st.c[0], c_jlo = st.c[1], c_llo = st.c[2], c_self = st.c[3];
+  const double c_lhi = st.c[4], c_jhi = st.c[5], c_ihi = st.c[6];
+  for (uint64_t u = u0; u < u1;) {
+    const uint32_t jbk = (uint32_t)(u / np), q0 = (uint32_t)(u % np);
+    const uint64_t qe = q0 + (u1 - u);
+    const uint32_t q1 = qe < np ? (uint32_t)qe : np;
+    u += q1 - q0;
+    const uint32_t j0 = jbk * jb, j = j0 + ty;
+    const bool act = ty < jb && j < k;
+    // lines [jlo, jhi) of a plane exist; they land at line (jlo - j0 + 1) of the buffer
+    const uint32_t jlo = j0 > 0 ? j0 - 1 : 0, jhi = min(j0 + jb + 1, k);
+    const uint32_t bytes = (jhi - jlo) * k * 8;
+    auto issue = [&](int q) {  // every thread: count the load; thread 0 issues it
+      const int b = (q + kMarchRing) % kMarchRing;
+      pbits ^= 1u << b;
+      if (threadIdx.x == 0) {
+        ptx::fence_proxy_async_smem();  // earlier generic reads of the buffer before the async write
+        ptx::mbar_arrive_expect_tx(&full[b], bytes);
+        ptx::bulk_g2s(buf(q) + (size_t)(jlo + 1 - j0) * k, plane(q) + (size_t)jlo * k, bytes, &full[b]);
+      }
+    };
+    const int base = exists((int)q0 - 1) ? (int)q0 - 1 : (int)q0;
+    for (int q = base; q < base + kMarchRing && q <= (int)q1; ++q)
+      if (exists(q)) issue(q);
+    const bool has_jlo = j > 0, has_jhi = j + 1 < k;
+    const uint32_t me = (ty + 1) * k + tx;  // point (j, tx) inside a plane buffer
+    double prv[PT] = {}, cur[PT], nxt[PT] = {};
+    if (base < (int)q0) {
+      wait(base);
+#pragma unroll
+      for (int t = 0; t < PT; ++t) prv[t] = act ? buf(base)[me + G * t] : 0.0;
+    }
+    wait((int)q0);
+#pragma unroll
+    for (int t = 0; t < PT; ++t) cur[t] = act ? buf((int)q0)[me + G * t] : 0.0;
+    if (base < (int)q0) {
+      __syncthreads();  // plane q0 - 1 is in registers: its buffer takes plane q0 + 3
+      if ((int)q0 + 3 <= (int)q1 && exists((int)q0 + 3)) issue((int)q0 + 3);
+    }
+    for (uint32_t q = q0; q < q1; ++q) {
+      const uint32_t gi = ip0 + q;
+      const bool has_ilo = gi > 0, has_ihi = gi + 1 < k;
+      if (has_ihi) wait((int)q + 1);
+      if (act) {
+        const double* pc = buf((int)q) + me;
+        const double* pn = buf((int)q + 1) + me;
+        double out[PT];
+        // interior lines of interior planes: every term present except l - 1 at
+        // l = 0 (t = 0, tx = 0) and l + 1 at l = k - 1 (t = PT - 1, tx = G - 1)
+        const bool inner = has_ilo && has_ihi && has_jlo && has_jhi;
+        if (inner) {
+#pragma unroll
+          for (int t = 0; t < PT; ++t) {
+            nxt[t] = pn[G * t];
+            const double jl = pc[G * t - k], jh = pc[G * t + k];
+            const bool lo = t > 0 || tx > 0, hi = t < PT - 1 || tx + 1 < G;
+            const double lm = lo ? pc[G * t - 1] : 0.0, lp = hi ? pc[G * t + 1] : 0.0;
+            double s = __dadd_rn(0.0, __dmul_rn(c_ilo, prv[t]));
+            s = __dadd_rn(s, __dmul_rn(c_jlo, jl));
+            if (lo) s = __dadd_rn(s, __dmul_rn(c_llo, lm));
+            s = __dadd_rn(s, __dmul_rn(c_self, cur[t]));
+            if (hi) s = __dadd_rn(s, __dmul_rn(c_lhi, lp));
+            s = __dadd_rn(s, __dmul_rn(c_jhi, jh));
+            out[t] = __dadd_rn(s, __dmul_rn(c_ihi, nxt[t]));
+          }
+        } else {
+#pragma unroll
+          for (int t = 0; t < PT; ++t) {
+            const uint32_t l = tx + G * t;
+            nxt[t] = has_ihi ? pn[G * t] : 0.0;
+            const double jl = has_jlo ? pc[G * t - k] : 0.0, jh = has_jhi ? pc[G * t + k] : 0.0;
+            const double lm = l > 0 ? pc[G * t - 1] : 0.0, lp = l + 1 < k ? pc[G * t + 1] : 0.0;
+            double s = 0.0;
+            if (has_ilo) s = __dadd_rn(s, __dmul_rn(c_ilo, prv[t]));
+            if (has_jlo) s = __dadd_rn(s, __dmul_rn(c_jlo, jl));
+            if (l > 0) s = __dadd_rn(s, __dmul_rn(c_llo, lm));
+            s = __dadd_rn(s, __dmul_rn(c_self, cur[t]));
+            if (l + 1 < k) s = __dadd_rn(s, __dmul_rn(c_lhi, lp));
+            if (has_jhi) s = __dadd_rn(s, __dmul_rn(c_jhi, jh));
+            if (has_ihi) s = __dadd_rn(s, __dmul_rn(c_ihi, nxt[t]));
+            out[t] = s;
+          }
+        }
+        double* yq = y + (size_t)q * kk + (size_t)j * k + tx;
+#pragma unroll
+        for (int t = 0; t < PT; ++t) yq[G * t] = out[t];
+      }
+#pragma unroll
+      for (int t = 0; t < PT; ++t) {
+        prv[t] = cur[t];
+        cur[t] = nxt[t];
+      }
+      __syncthreads();  // every read of plane q is done: its buffer takes plane q + 4
+      if ((int)q + 4 <= (int)q1 && exists((int)q + 4)) issue((int)q + 4);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // wide Count stages (thousands of buckets, e.g. count_gauss at shat = 60:
 // 7442): bucket-sorted application
@@ -811,7 +957,44 @@ int op_apply(bo_op op, const double* x, double* y, bo_status* st) {
   else {
     Stencil stc;
     for (int q = 0; q < 7; ++q) stc.c[q] = op->coef[q];
-    if (st4) {
+    // plane-marching 3-D kernel: whole planes per shard, halos of one plane
+    static const bool march_on = [] {
+      const char* e = getenv("BO_SPMV_MARCH");
+      return !(e && atoi(e) == 0);
+    }();
+    const uint64_t kk = op->k * op->k;
+    const bool march = march_on && st4 && op->dims == 3 && op->k <= 512 && ctx->row_begin % kk == 0 &&
+                       nl % (long long)kk == 0 && (op->halo_lo == 0 || op->halo_lo == kk) &&
+                       (op->halo_hi == 0 || op->halo_hi == kk);
+    if (march) {
+      // four points per thread, 256 threads (k = 200: five lines per CTA, four
+      // CTAs per SM).  Measured at n = 8e6 (scripts/prof_spmv.py): 30.7 us per
+      // SpMV; eight points per thread (BO_SPMV_PT=8, ten lines: fewer halo
+      // reads) 36.7 us, 384 / 512-thread CTAs 31.2 / 32.5 us, the 4-row
+      // kernel below 38 us.
+      static const int pt_env = [] {
+        const char* e = getenv("BO_SPMV_PT");
+        return e ? atoi(e) : 0;
+      }();
+      const uint32_t k = (uint32_t)op->k;
+      static const int tpb_env = [] {
+        const char* e = getenv("BO_SPMV_TPB");
+        return e ? atoi(e) : 256;
+      }();
+      const uint32_t PT = (pt_env == 8 && k % 8 == 0 && k >= 64) ? 8 : 4, G = k / PT;
+      const uint32_t jb = std::max<uint32_t>(1, std::min<uint32_t>((uint32_t)std::min(512, tpb_env) / G, k));
+      const uint32_t nbj = (k + jb - 1) / jb, np = (uint32_t)(nl / (long long)kk);
+      const size_t smem = (size_t)kMarchRing * (jb + 2) * k * 8;
+      // persistent grid: as many CTAs as fit on the SMs at once, equal shares
+      const uint32_t per_sm = (uint32_t)std::max<size_t>(1, std::min<size_t>(4, (220 * 1024) / smem));
+      const uint32_t grid_m = std::max<uint32_t>(1, std::min<uint32_t>(nbj * np, (uint32_t)ctx->num_sms * per_sm));
+      const double* hlo = op->xext ? op->xext + op->halo_lo - kk : x;  // the plane below (when it exists)
+      const double* hhi = op->xext ? op->xext + op->halo_lo + nl : x;
+      auto kfn = PT == 8 ? spmv_stencil7_march_kernel<8> : spmv_stencil7_march_kernel<4>;
+      if (smem > 48 * 1024)
+        CU(cudaFuncSetAttribute((const void*)kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kfn<<<grid_m, G * jb, smem, ctx->stream>>>(k, jb, (uint32_t)(ctx->row_begin / kk), np, stc, x, hlo, hhi, y);
+    } else if (st4) {
       const uint32_t ng = (uint32_t)(nl / 4);
       // one 4-row group per thread, no grid-stride loop: as many loads in
       // flight as the SMs hold (ncu: the capped grid was latency-bound)

@@ -31,6 +31,12 @@
 #ifndef BO_GAW
 #define BO_GAW 2  // row-solve warps of pre-solve passes; 0: NW - 4 (see pass_kernel)
 #endif
+#ifndef BO_GAW_QTX
+#define BO_GAW_QTX BO_GAW  // ... of the pre-solve projection passes (P2_QTX)
+#endif
+#ifndef BO_GAW_UPD
+#define BO_GAW_UPD BO_GAW  // ... of the pre-solve update passes (P2_UPD_*)
+#endif
 #include "bo_tiny.cuh"
 
 // Phase profiler (diagnostic builds only): lane 0 of every consumer warp
@@ -297,17 +303,18 @@ __device__ __forceinline__ void row_trsm_n(double (&x)[NR][kMaxK], const double*
 // the number of 8-column tiles is dispatched to a compile-time constant.
 template <int NT, int T, int NPRE, bool UPD, int NPOST, bool QTX, bool GRAM, int SK, bool STORE, bool EXACT,
           int KC = 0>
-__global__ void __launch_bounds__(pass_threads(UPD), 1)
+__global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 && UPD), 1)
     pass_kernel(const __grid_constant__ PassArgs a, const __grid_constant__ CUtensorMap tmV,
                 const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmT) {
   constexpr int S = TileGeom<T>::S;
   constexpr int NSUB = TileGeom<T>::NSUB;  // 128-row sub-tiles per tile (T = 256: 2)
-  constexpr int NW = consumer_warps(UPD);
+  constexpr int NW = consumer_warps(UPD, NPRE > 0 && QTX, NPRE > 0 && UPD);
   constexpr bool SPLIT = NPRE > 0;
   // Row-solve warps.  Two, by measurement: NW - 4 (one U/S/R warp per SM
   // sub-partition) was 3% slower over the C2 sequence, since the update is
   // bound by the shared FP64 pipe, not by which sub-partition issues it.
-  constexpr int GAW = SPLIT ? (BO_GAW > 0 ? BO_GAW : NW - 4) : 0;
+  constexpr int GAW0 = (NPRE > 0 && QTX) ? BO_GAW_QTX : (NPRE > 0 && UPD) ? BO_GAW_UPD : BO_GAW;
+  constexpr int GAW = SPLIT ? (GAW0 > 0 ? GAW0 : NW - 4) : 0;
   constexpr int GW = NW - GAW;             // warps of the U/S/R group
   constexpr int GT = GW * 32;
   constexpr int GBAR = SPLIT ? 6 : 1;      // named barrier of the U/S/R group

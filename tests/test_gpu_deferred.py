@@ -136,3 +136,34 @@ def test_gmres_bitwise_reproducible(gpu):
         ctx.close()
     assert np.array_equal(outs[0][0], outs[1][0])
     assert outs[0][1] == outs[1][1] and outs[0][2] == outs[1][2]
+
+
+def test_import_ordered_before_next_pass(gpu):
+    """bo_basis_import (the reference driver's store re-import after every
+    restart and recover_panel) must land before the next pass reads the slab.
+    A pageable cudaMemcpy on the legacy stream may return before its DMA is
+    done and the non-blocking ctx stream does not wait for it; with 320 MB
+    per import the projection right after it saw the old slab contents."""
+    import ctypes as C
+
+    from paper_2503_16717_b200 import _lib as L
+    n, cols, k = 2_000_000, 20, 4
+    ctx = gpu.Context(n)
+    st = gpu.BasisStore(ctx, cols + k)
+    rng = np.random.default_rng(5)
+    v = ctx.from_host(rng.standard_normal((n, k)))
+    vh = ctx.to_host(v)
+    dp = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
+    r = np.eye(cols)
+    bounds = np.array([0, cols], dtype=np.uint64)
+    for trial in range(4):
+        q = np.asfortranarray(rng.standard_normal((n, cols)))
+        stc = L.Status()
+        rc = ctx.lib.bo_basis_import(st.h, cols, dp(q), n, dp(np.asfortranarray(r)), None, None,
+                                     bounds.ctypes.data_as(C.POINTER(C.c_uint64)), 2, C.byref(stc))
+        assert rc == 0
+        got = gpu.borth.bcgs_project(st, v).coeffs
+        want = q.T @ vh
+        err = np.max(np.abs(got - want)) / np.max(np.abs(want))
+        assert err < 1e-12, (trial, err)
+    ctx.close()

@@ -25,7 +25,9 @@ def mk(gpu):
 
 
 # ------------------------------------------------------------- SpMV / MPK --
-@pytest.mark.parametrize("dims,k", [(2, 100), (3, 20), (2, 7), (3, 33)])
+# 3-D k % 4 == 0: the plane-marching kernel (k = 12: one CTA column; 200: the
+# C3 grid); k = 33: the generic kernel
+@pytest.mark.parametrize("dims,k", [(2, 100), (3, 20), (2, 7), (3, 33), (3, 12), (3, 64), (3, 200)])
 def test_spmv_laplace_bit_exact(gpu, mk, orc, dims, k):
     csr = orc.laplace(k, dims)
     n = len(csr[0]) - 1
@@ -64,13 +66,13 @@ def test_spmv_random_csr(gpu, mk, orc):
     assert np.array_equal(y, orc.spmv(csr, x))
 
 
-@pytest.mark.parametrize("s", [5, 10])
-def test_mpk_bit_exact(gpu, mk, orc, s):
-    csr = orc.laplace(30, 3)
+@pytest.mark.parametrize("s,side", [(5, 30), (10, 30), (10, 40)])
+def test_mpk_bit_exact(gpu, mk, orc, s, side):
+    csr = orc.laplace(side, 3)
     n = len(csr[0]) - 1
     ctx = mk(n)
     v0 = np.random.default_rng(s).standard_normal(n)
-    v = ctx.to_host(gpu.Operator.laplace(ctx, 3, 30).mpk(ctx.from_host(v0), s))
+    v = ctx.to_host(gpu.Operator.laplace(ctx, 3, side).mpk(ctx.from_host(v0), s))
     assert np.array_equal(v, orc.mpk(csr, v0, s))
 
 
