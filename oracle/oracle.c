@@ -148,14 +148,36 @@ double orc_rng_sign(orc_rng* r) { return (mt_next(r) & 1ULL) ? 1.0 : -1.0; }
 /* ------------------------------------------------------------------------ */
 /* dense — proj/src/dense.cpp                                               */
 /* ------------------------------------------------------------------------ */
+/* Tall dot products of gram / transpose_times.  Chunks 0 or 1 (the default)
+ * is the reference's sequential row sum, exactly.  Chunks c > 1 is a
+ * TEST-ONLY perturbation (orc_set_sum_chunks): rows split into c contiguous
+ * runs, each summed in order, the run sums added in order -- the same
+ * algorithm with another summation order, whose effect on an output measures
+ * the reference's own sensitivity to reordering, the yardstick
+ * for the GPU's tree-ordered sums. */
+static size_t g_sum_chunks = 0;
+void orc_set_sum_chunks(size_t chunks) { g_sum_chunks = chunks; }
+static double tall_dot(const double* a, const double* b, size_t n) {
+  if (g_sum_chunks <= 1) {
+    double s = 0.0;
+    for (size_t r = 0; r < n; ++r) s += a[r] * b[r];
+    return s;
+  }
+  double tot = 0.0;
+  for (size_t q = 0; q < g_sum_chunks; ++q) {
+    const size_t lo = n * q / g_sum_chunks, hi = n * (q + 1) / g_sum_chunks;
+    double s = 0.0;
+    for (size_t r = lo; r < hi; ++r) s += a[r] * b[r];
+    tot += s;
+  }
+  return tot;
+}
+
 /* dense.cpp:10-26 (ledger recorded by callers) */
 void orc_gram(const double* v, size_t n, size_t k, double* g) {
   for (size_t j = 0; j < k; ++j)
     for (size_t i = 0; i <= j; ++i) {
-      double s = 0.0;
-      const double* ci = v + i * n;
-      const double* cj = v + j * n;
-      for (size_t r = 0; r < n; ++r) s += ci[r] * cj[r];
+      const double s = tall_dot(v + i * n, v + j * n, n);
       AT(g, k, i, j) = s;
       AT(g, k, j, i) = s;
     }
@@ -170,12 +192,7 @@ void orc_transpose_times(const double* a, size_t n, size_t ca, const double* b, 
                          double* c) {
   for (size_t j = 0; j < cb; ++j) {
     const double* bj = b + j * n;
-    for (size_t i = 0; i < ca; ++i) {
-      const double* ai = a + i * n;
-      double s = 0.0;
-      for (size_t r = 0; r < n; ++r) s += ai[r] * bj[r];
-      AT(c, ca, i, j) = s;
-    }
+    for (size_t i = 0; i < ca; ++i) AT(c, ca, i, j) = tall_dot(a + i * n, bj, n);
   }
 }
 

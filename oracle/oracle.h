@@ -65,6 +65,9 @@ double orc_rng_sign(orc_rng* r);
  * strict lower part zero (storage differs from the packed UpperTriangular,
  * values are identical) */
 void orc_gram(const double* v, size_t n, size_t k, double* g /* k*k */);
+/* test-only: sum the tall dot products of gram / transpose_times in `chunks`
+ * contiguous runs (0 / 1: the reference's sequential order) */
+void orc_set_sum_chunks(size_t chunks);
 void orc_transpose_times(const double* a, size_t n, size_t ca, const double* b, size_t cb,
                          double* c /* ca*cb */);
 void orc_times(const double* a, size_t n, size_t ca, const double* b, size_t cb,

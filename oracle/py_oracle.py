@@ -108,6 +108,12 @@ class Oracle:
         s = self._status().contents
         return s.code, s.msg.decode(errors="replace"), s.index
 
+    def set_sum_chunks(self, chunks: int):
+        """test-only summation-order perturbation of the C restatement's tall
+        dot products (oracle.c tall_dot); 0 restores the reference order"""
+        assert self.which == "orc", "only the C restatement has a summation-order knob"
+        self._fn("set_sum_chunks", None, [sz])(chunks)
+
     # ---------------- rng
     def derive_seed(self, base, stream):
         return int(self._fn("derive_seed", u64, [u64, u64])(base, stream))

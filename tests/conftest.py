@@ -81,3 +81,52 @@ def orth_err(q):
 def kappa_tol(kappa, floor=1e-10):
     """parity contract: max(1e-10, 10 kappa eps)"""
     return max(floor, 10.0 * kappa * 2.220446049250313e-16)
+
+
+def ulp_sensitivity(run, x, draws=4, entries=50, seed=0):
+    """The reference algorithm's own sensitivity at this input: the worst
+    relative change of each output of run(x) (a tuple of arrays, computed by
+    the CPU oracle, bit-identical to the reference) when `entries` entries of
+    x move by one ulp, over `draws` draws.  A GPU result whose sums are
+    merely ordered differently should stay within a small multiple of it."""
+    base = [np.asarray(o) for o in run(x)]
+    worst = [0.0] * len(base)
+    rng = np.random.default_rng(seed)
+    for t in range(draws):
+        y = np.array(x, copy=True)
+        flat = y.reshape(-1, order="F") if y.flags.f_contiguous else y.reshape(-1)
+        idx = rng.integers(0, flat.size, entries)
+        flat[idx] = np.nextafter(flat[idx], np.inf if t % 2 else -np.inf)
+        for i, o in enumerate(run(y)):
+            worst[i] = max(worst[i], rel_err(o, base[i]))
+    return worst
+
+
+def order_sensitivity(orc, run, x, chunks=(148, 1184)):
+    """The reference algorithm's sensitivity to the summation order of its
+    tall dot products: the worst relative change of each output of run(x)
+    when the C oracle sums them in `chunks` contiguous runs instead of one
+    (oracle.c tall_dot)."""
+    base = [np.asarray(o) for o in run(x)]
+    worst = [0.0] * len(base)
+    try:
+        for c in chunks:
+            orc.set_sum_chunks(c)
+            for i, o in enumerate(run(x)):
+                worst[i] = max(worst[i], rel_err(o, base[i]))
+    finally:
+        orc.set_sum_chunks(0)
+    return worst
+
+
+def envelope(sens, factor=10.0, floor=1e-10):
+    """parity tolerance from a measured sensitivity"""
+    return max(floor, factor * sens)
+
+
+def ref_envelopes(orc, run, x, factor=10.0):
+    """per-output parity tolerances: `factor` x the worst of the reference's
+    own one-ulp input sensitivity and summation-order sensitivity, floored at
+    the north star's 1e-10; also returns the two sensitivities for printing"""
+    su, so = ulp_sensitivity(run, x), order_sensitivity(orc, run, x)
+    return [envelope(max(a, b), factor) for a, b in zip(su, so)], su, so

@@ -5,7 +5,7 @@ from pathlib import Path
 import numpy as np
 import pytest
 
-from conftest import kappa_tol, orth_err, rel_err
+from conftest import kappa_tol, orth_err, ref_envelopes, rel_err
 
 pytestmark = pytest.mark.gpu
 
@@ -194,7 +194,20 @@ def orc_total(orc, ob):
     return sum(orc.basis_ledger(ob))
 
 
+def _two_stage_oracle(orc, v, n, k, panels_per_big, bigs, preproc):
+    ob = orc.basis_new(n, panels_per_big * bigs * k + 1)
+    for bi in range(bigs):
+        orc.basis_begin_big_panel(ob, 0, 0)
+        for pi in range(panels_per_big):
+            c0 = (bi * panels_per_big + pi) * k
+            assert orc.two_stage_panel(ob, v[:, c0:c0 + k], preproc, None).code == 0
+        assert orc.two_stage_finish(ob, preproc).code == 0
+    return ob
+
+
 def test_two_stage_pip_well_conditioned(gpu, mk, orc):
+    """two-stage BCGS-PIP: Q and R within 10x the reference's own one-ulp
+    sensitivity on this input (PIP squares the condition number)"""
     n, k = 20000, 5
     v = orc.gen_glued(n, 24, k, 1e2, 1e3, 5)
     ctx = mk(n)
@@ -203,8 +216,17 @@ def test_two_stage_pip_well_conditioned(gpu, mk, orc):
     q = st.basis_copy()
     assert orth_err(q) < 1e-12
     qo, _, _ = orc.basis_state(ob, n)
-    assert rel_err(q, qo) < 1e-7
-    assert rel_err(st.r_copy(), orc.basis_r(ob, 24 * k + 1)) < 1e-7
+
+    def run(x):
+        o = _two_stage_oracle(orc, x, n, k, 6, 4, 0)
+        return orc.basis_state(o, n)[0], orc.basis_r(o, 24 * k + 1)
+
+    tol, su, so = ref_envelopes(orc, run, v)
+    d_q, d_r = rel_err(q, qo), rel_err(st.r_copy(), orc.basis_r(ob, 24 * k + 1))
+    print(f"two-stage PIP: Q rel. delta {d_q:.1e} (ref. one-ulp / order sensitivity {su[0]:.1e} / {so[0]:.1e}), "
+          f"R {d_r:.1e} ({su[1]:.1e} / {so[1]:.1e})")
+    assert d_q <= tol[0]
+    assert d_r <= tol[1]
 
 
 # ---------------------------------------------------------------- GMRES --
@@ -233,7 +255,9 @@ def _gmres(gpu, mk, orc, k2d, **kw):
 # restart 5, 1.9e-9 at 6-7) and (c) glibc's FMA / non-FMA libm variants
 # (scripts/isa_envelope.py; two-stage RandBCGS 6.1e-9, 3.6e-7, 7.7e-4, 1.3e-3
 # at restarts 6-9), floored at the north star's 1e-10.
-C1_ENVELOPE = [1e-10, 1.7e-10, 3.8e-10, 5.7e-10, 8.3e-10, 8.3e-10, 5.2e-7, 3.0e-5, 9.1e-3, 1.7e-2]
+# Through restart 5 the north star's 1e-10 is the
+# bound: the measured GPU deltas there are <= 3.2e-11 (config 1, both schemes).
+C1_ENVELOPE = [1e-10, 1e-10, 1e-10, 1e-10, 1e-10, 1e-10, 5.2e-7, 3.0e-5, 9.1e-3, 1.7e-2]
 
 
 def _envelope(i, scheme=None):
@@ -356,7 +380,10 @@ def test_gmres_c3_cholqr2_full_size(gpu, mk):
     assert (rep["restarts"], rep["iterations"]) == (want["restarts"], want["iterations"]) == (1, 10)
     assert rep["reduce"] == want["reduce"] == [2, 4, 0, 2]
     assert abs(rep["final_relres"] - want["final_relres"]) <= 1e-10 * want["final_relres"]
-    assert abs(rep["restart_lsq_residual"][0] - want["lsq"][0]) <= 1e-8 * want["lsq"][0]
+    d_lsq = abs(rep["restart_lsq_residual"][0] - want["lsq"][0]) / want["lsq"][0]
+    print(f"c3 cholqr2: relres rel. delta {abs(rep['final_relres'] - want['final_relres']) / want['final_relres']:.1e}, "
+          f"LSQ residual {d_lsq:.1e}")
+    assert d_lsq <= 1e-10
 
 
 def test_gmres_c1_from_matrix_market(gpu, mk, orc, tmp_path):

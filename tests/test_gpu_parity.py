@@ -6,7 +6,7 @@ breakdown steps and messages."""
 import numpy as np
 import pytest
 
-from conftest import kappa_tol, orth_err, rel_err, ulps
+from conftest import kappa_tol, orth_err, ref_envelopes, rel_err, ulps
 
 pytestmark = pytest.mark.gpu
 
@@ -315,36 +315,48 @@ def test_bcgs2_ledger_contract(gpu, mk, orc):
 
 
 def test_bcgs2_overlap_vs_oracle(gpu, mk, orc):
-    """GMRES-shaped sequence: each panel's first column is the current last basis column."""
-    n, s = 30000, 5
-    k = s + 1
-    rp, ci, vv = orc.laplace(int(round(n ** 0.5)) + 0, 2) if False else orc.laplace(173, 2)
+    """GMRES-shaped sequence: each panel's first column is the current last
+    basis column.  R and the input coefficient columns within 10x the
+    reference's own one-ulp sensitivity (seed vector perturbed, oracle re-run)."""
+    s = 5
+    rp, ci, vv = orc.laplace(173, 2)
     n = len(rp) - 1
-    ctx = mk(n)
-    st = gpu.BasisStore(ctx, 4 * s + 1)
-    ob = orc.basis_new(n, 4 * s + 1)
     rng = np.random.default_rng(0)
     q1 = rng.standard_normal(n)
     q1 /= np.linalg.norm(q1)
-    seed_vec = q1
-    for j in range(4):
-        if j > 0:
-            k0 = st.cols() - 1
-            st.mark_seed(k0)
-            orc.basis_mark_seed(ob, k0)
-            qo, _, _ = orc.basis_state(ob, n)
-            seed_vec = qo[:, k0]
-        v = orc.mpk((rp, ci, vv), seed_vec, s)
-        gpu.bcgs2(st, ctx.from_host(v), 0, None, overlap=j > 0)
-        assert orc.bcgs2(ob, v, 0, None, overlap=j > 0).code == 0
-    qo, _, lo = orc.basis_state(ob, n)
+
+    def run(seed, st=None, ctx=None):
+        ob = orc.basis_new(n, 4 * s + 1)
+        seed_vec = seed
+        for j in range(4):
+            if j > 0:
+                k0 = orc.basis_cols(ob) - 1
+                orc.basis_mark_seed(ob, k0)
+                if st is not None:
+                    st.mark_seed(k0)
+                qo, _, _ = orc.basis_state(ob, n)
+                seed_vec = qo[:, k0]
+            v = orc.mpk((rp, ci, vv), seed_vec, s)
+            if st is not None:
+                gpu.bcgs2(st, ctx.from_host(v), 0, None, overlap=j > 0)
+            assert orc.bcgs2(ob, v, 0, None, overlap=j > 0).code == 0
+        cols = orc.basis_cols(ob)
+        coeffs = np.stack([orc.basis_input_coeff_col(ob, kk, cols) for kk in range(cols)], axis=1)
+        return ob, orc.basis_r(ob, cols), coeffs
+
+    ctx = mk(n)
+    st = gpu.BasisStore(ctx, 4 * s + 1)
+    ob, r_want, c_want = run(q1, st, ctx)
+    _, lo = orc.basis_state(ob, n)[1:]
     assert st.cols() == orc.basis_cols(ob) == 4 * s + 1
     assert st.ledger().counts == lo
-    assert rel_err(st.r_copy(), orc.basis_r(ob, 4 * s + 1)) < 1e-8
-    for kk in range(st.cols()):
-        want = orc.basis_input_coeff_col(ob, kk, st.cols())
-        got = st.input_coeff_col(kk, st.cols())
-        assert np.max(np.abs(got - want)) <= 1e-8 * np.max(np.abs(want))
+    tol, su, so = ref_envelopes(orc, lambda x: run(x)[1:], q1)
+    c_got = np.stack([st.input_coeff_col(kk, st.cols()) for kk in range(st.cols())], axis=1)
+    d_r, d_c = rel_err(st.r_copy(), r_want), rel_err(c_got, c_want)
+    print(f"overlap: R rel. delta {d_r:.1e} (ref. one-ulp / order sensitivity {su[0]:.1e} / {so[0]:.1e}), "
+          f"coefficients {d_c:.1e} ({su[1]:.1e} / {so[1]:.1e})")
+    assert d_r <= tol[0]
+    assert d_c <= tol[1]
 
 
 @pytest.mark.parametrize("kappa,step", [(1e10, 5), (1e14, 4)])

@@ -25,7 +25,8 @@ def refgpu(gpu):
     return Oracle("refgpu")
 
 
-C1_ENVELOPE = [1e-10, 1.7e-10, 3.8e-10, 5.7e-10, 8.3e-10, 8.3e-10, 5.2e-7, 3.0e-5, 9.1e-3, 1.7e-2]
+# tests/test_gpu_ops.py C1_ENVELOPE: the north star's 1e-10 through restart 5
+C1_ENVELOPE = [1e-10, 1e-10, 1e-10, 1e-10, 1e-10, 1e-10, 5.2e-7, 3.0e-5, 9.1e-3, 1.7e-2]
 
 
 @pytest.mark.parametrize("scheme", [0, 1])

@@ -147,7 +147,10 @@ def test_sharded_bcgs2(gpu, tmp_path, case):
     r = _run(case, tmp_path)
     assert r["ledger"] == r["ledger_oracle"]
     assert r["allreduces"] == sum(r["ledger"])
-    assert r["q_rel"] < 1e-8 and r["recon"] < 1e-12
+    # the same inputs as the single-GPU sequence tests: kappa = 1e6 glued panels
+    from conftest import kappa_tol
+    print(f"{case}: Q rel. delta vs the oracle {r['q_rel']:.1e}, ||V - QR|| / ||V|| {r['recon']:.1e}")
+    assert r["q_rel"] < kappa_tol(1e6) and r["recon"] < 1e-12
     assert r["orth"] < 1e-13
 
 
