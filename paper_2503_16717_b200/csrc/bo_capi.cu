@@ -377,7 +377,10 @@ int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st) {
     if (ctx->world > 1 && (ki.qtx || ki.gram || ki.sk != SK_NONE))
       TRY(comm_allreduce(ctx, ctx->sums, (size_t)a.part_len, st));
     if (f.ops) {
-      finalize_kernel<<<1, 256, 0, ctx->stream>>>(f);
+      const size_t fsm = (1536 + (size_t)std::max(f.mh, 32) * 16 + 64) * 8;
+      if (fsm > 48 * 1024)
+        CU(cudaFuncSetAttribute((const void*)finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
+      finalize_kernel<<<1, 256, fsm, ctx->stream>>>(f);
       CU(cudaGetLastError());
       ctx->launches++;
     }
@@ -478,10 +481,12 @@ int reset_status(bo_ctx ctx, bo_status* st) {
 }
 // fetch status + tiny workspace to host
 int fetch(bo_ctx ctx, bool tiny, bo_status* st) {
-  CU(cudaMemcpyAsync(ctx->status_host, ctx->status, sizeof(DevStatus), cudaMemcpyDeviceToHost, ctx->stream));
-  if (tiny)
+  if (tiny)  // the status word leads the workspace: one copy
     CU(cudaMemcpyAsync(ctx->tiny_host, ctx->tiny, TINY_LEN * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  else
+    CU(cudaMemcpyAsync(ctx->status_host, ctx->status, sizeof(DevStatus), cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
+  if (tiny) std::memcpy(ctx->status_host, ctx->tiny_host + OFF_STATUS, sizeof(DevStatus));
   return BO_OK;
 }
 
@@ -592,12 +597,12 @@ static int ctx_create_impl(int device, int rank, int world, const void* nccl_id,
   }
   CU(cudaMalloc(&c->counter, bo::kMaxRedCounters * sizeof(unsigned)));
   CU(cudaMemset(c->counter, 0, bo::kMaxRedCounters * sizeof(unsigned)));
-  CU(cudaMalloc(&c->status, sizeof(DevStatus)));
-  CU(cudaMemset(c->status, 0, sizeof(DevStatus)));
+
   CU(cudaMallocHost(&c->status_host, sizeof(DevStatus)));
   c->tiny_cap = TINY_LEN;
   CU(cudaMalloc(&c->tiny, TINY_LEN * 8));
   CU(cudaMemset(c->tiny, 0, TINY_LEN * 8));
+  c->status = reinterpret_cast<DevStatus*>(c->tiny + OFF_STATUS);  // leads the workspace (one-copy snapshots)
   CU(cudaMallocHost(&c->tiny_host, TINY_LEN * 8));
   for (int i = 0; i < 3; ++i) {
     CU(cudaMalloc(&c->scratch[i], c->ld * 16 * 8));
@@ -636,7 +641,6 @@ extern "C" int bo_ctx_destroy(bo_ctx c) {
   cudaFree(c->phase_prof);
   cudaFree(c->sums);
   cudaFree(c->counter);
-  cudaFree(c->status);
   cudaFreeHost(c->status_host);
   cudaFree(c->tiny);
   cudaFreeHost(c->tiny_host);
@@ -1314,7 +1318,6 @@ extern "C" int bo_basis_destroy(bo_basis b) {
   if (!b) return BO_OK;
   basis_drain(b);
   if (b->snap) cudaFreeHost(b->snap);
-  if (b->snap_st) cudaFreeHost(b->snap_st);
   cudaStreamSynchronize(b->ctx->stream);
   cudaFree(b->q);
   delete b;
@@ -1581,20 +1584,12 @@ namespace host {
 // its host bookkeeping needs (Rin for a first panel; coefficients and R_jj)
 int snapshot(bo_basis b, bo_basis_s::Pending& op, bo_status* st) {
   bo_ctx ctx = b->ctx;
-  if (!b->snap) {
-    CU(cudaMallocHost((void**)&b->snap, (size_t)kSnapSlots * kSnapLen * 8));
-    CU(cudaMallocHost((void**)&b->snap_st, (size_t)kSnapSlots * sizeof(DevStatus)));
-  }
+  if (!b->snap) CU(cudaMallocHost((void**)&b->snap, (size_t)kSnapSlots * kSnapLen * 8));
   op.slot = b->nsnap++;
   double* sn = b->snap + (size_t)op.slot * kSnapLen;
-  CU(cudaMemcpyAsync(&b->snap_st[op.slot], ctx->status, sizeof(DevStatus), cudaMemcpyDeviceToHost, ctx->stream));
-  if (op.first) {
-    CU(cudaMemcpyAsync(sn + kSnapRin, ctx->tiny + OFF_RIN, 256 * 8, cudaMemcpyDeviceToHost, ctx->stream));
-  } else {
-    CU(cudaMemcpyAsync(sn + kSnapCoef, ctx->tiny + OFF_COEF, (size_t)LDC * 16 * 8, cudaMemcpyDeviceToHost,
-                       ctx->stream));
-    CU(cudaMemcpyAsync(sn + kSnapRjj, ctx->tiny + OFF_RJJ, 256 * 8, cudaMemcpyDeviceToHost, ctx->stream));
-  }
+  // one copy of [status | Rin] (first panel) or [status | Rin | R_jj | coefficients]
+  const size_t len = op.first ? (size_t)OFF_RJJ : (size_t)kSnapLen;
+  CU(cudaMemcpyAsync(sn, ctx->tiny + OFF_STATUS, len * 8, cudaMemcpyDeviceToHost, ctx->stream));
   b->pend.push_back(op);
   b->cols = op.cols_before - (op.overlap ? 1 : 0) + op.k;  // speculative: as if the call succeeds
   return BO_OK;
@@ -1791,7 +1786,8 @@ extern "C" int bo_basis_sync(bo_basis b, uint64_t* failed, bo_status* st) {
       b->seeded[op.col] = 1;
       continue;
     }
-    const DevStatus& d = b->snap_st[op.slot];
+    DevStatus d;
+    std::memcpy(&d, b->snap + (size_t)op.slot * kSnapLen + kSnapStatus, sizeof d);
     const double* sn = b->snap + (size_t)op.slot * kSnapLen;
     // ledger: the reduce events the call reached (block_orth.cpp:212-221)
     if (op.first) {

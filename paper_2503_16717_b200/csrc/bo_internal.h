@@ -109,7 +109,6 @@ struct bo_basis_s {
   };
   std::vector<Pending> pend;
   double* snap = nullptr;            // pinned [kSnapSlots][kSnapLen]
-  bo::DevStatus* snap_st = nullptr;  // pinned [kSnapSlots]
   int nsnap = 0;
   int deferred_code = 0;             // first failure drained by an accessor, reported by the next sync
   bo_status deferred_st{};
@@ -203,11 +202,18 @@ struct PassReq {
 // tiny workspace layout (doubles) — all K x K factors have ld 16
 // projection coefficient blocks (p x K) have ld LDC = 256 (p <= 255 basis columns)
 constexpr int LDC = 256;
-// deferred-call snapshots (bo_bcgs2_enqueue): Rin | R_jj | coefficients
-constexpr int kSnapSlots = 64, kSnapRin = 0, kSnapRjj = 256, kSnapCoef = 512, kSnapLen = 512 + LDC * 16;
-constexpr int OFF_R1 = 0, OFF_R2 = 256, OFF_R3 = 512, OFF_RIN = 768, OFF_RJJ = 1024,
-              OFF_G = 1280, OFF_R4 = 1536, OFF_C1 = 2048, OFF_C2 = OFF_C1 + LDC * 16,
-              OFF_COEF = OFF_C2 + LDC * 16, OFF_S = OFF_COEF + LDC * 16, TINY_LEN = OFF_S + 8192;
+// The device status word and the factors a deferred call's host bookkeeping
+// needs (Rin of a first panel; R_jj and the coefficients otherwise) lead the
+// workspace contiguously, so a call's snapshot is ONE device-to-host copy.
+constexpr int OFF_STATUS = 0, OFF_RIN = 8, OFF_RJJ = OFF_RIN + 256, OFF_COEF = OFF_RJJ + 256,
+              OFF_R1 = OFF_COEF + LDC * 16, OFF_R2 = OFF_R1 + 256, OFF_R3 = OFF_R2 + 256, OFF_G = OFF_R3 + 256,
+              OFF_R4 = OFF_G + 256, OFF_C1 = OFF_R4 + 512, OFF_C2 = OFF_C1 + LDC * 16, OFF_S = OFF_C2 + LDC * 16,
+              TINY_LEN = OFF_S + 8192;
+static_assert(sizeof(bo::DevStatus) <= OFF_RIN * sizeof(double), "status word slot");
+// deferred-call snapshots (bo_bcgs2_enqueue): the leading workspace block
+// [status | Rin | R_jj | coefficients], copied as one range
+constexpr int kSnapSlots = 64, kSnapStatus = OFF_STATUS, kSnapRin = OFF_RIN, kSnapRjj = OFF_RJJ,
+              kSnapCoef = OFF_COEF, kSnapLen = OFF_COEF + LDC * 16;
 
 // NCCL, loaded lazily with dlopen (prefers the copy torch already mapped)
 struct NcclApi {

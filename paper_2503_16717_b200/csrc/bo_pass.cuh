@@ -196,9 +196,11 @@ static __device__ void finalize_dev(const FinArgs& f, double* smem_scratch /* >=
   __syncthreads();
 }
 
+// dynamic shared memory: (1536 + max(mh, 32) * 16 + 64) doubles (the sketch
+// block of a Count sketch has one row per bucket)
 static __global__ void __launch_bounds__(256) finalize_kernel(FinArgs f) {
-  __shared__ double scratch[1536 + 32 * 16];
-  finalize_dev(f, scratch);
+  extern __shared__ __align__(16) double fin_scratch[];
+  finalize_dev(f, fin_scratch);
 }
 
 
@@ -368,7 +370,6 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
   __shared__ int s_skip;
 
   if (tid == 0) {
-    s_skip = a.status->code != ST_OK;
     for (int s = 0; s < NS; ++s) {
       ptx::mbar_init(&full[s], 1);
       if (SPLIT) ptx::mbar_init(&solved[s], GAW);
@@ -377,12 +378,6 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
     }
     ptx::fence_mbar_init();
   }
-  if (NPRE > 0)
-    for (int e = tid; e < 256; e += blockDim.x) rfac[e] = a.Rpre0[e];
-  if (NPRE > 1)
-    for (int e = tid; e < 256; e += blockDim.x) rfac[256 + e] = a.Rpre1[e];
-  if (NPOST > 0)
-    for (int e = tid; e < 256; e += blockDim.x) rfac[512 + e] = a.Rpost[e];
   if (SK == SK_COUNT)
     for (int e = tid; e < mh * K; e += blockDim.x) cacc[e] = 0.0;
   // zero padding columns (never written by TMA or the phases)
@@ -396,6 +391,13 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
   if (XT && !ROWG && !XIN)
     for (int b = 0; b < 2 * NSUB; ++b)
       for (int e = tid; e < (KP - K) * S; e += blockDim.x) xtile[b * KP * S + K * S + e] = 0.0;
+  if (tid == 0) s_skip = a.status->code != ST_OK;
+  if (NPRE > 0)
+    for (int e = tid; e < 256; e += blockDim.x) rfac[e] = a.Rpre0[e];
+  if (NPRE > 1)
+    for (int e = tid; e < 256; e += blockDim.x) rfac[256 + e] = a.Rpre1[e];
+  if (NPOST > 0)
+    for (int e = tid; e < 256; e += blockDim.x) rfac[512 + e] = a.Rpost[e];
   __syncthreads();
   if (tid < 48) {
     const int f = tid / 16, j = tid % 16;

@@ -20,68 +20,57 @@ __device__ __forceinline__ double div(double a, double b) { return __ddiv_rn(a, 
 // subtractions in the same order (t = 0, 1, ...), so it is bit-identical.
 // On failure at 1-based step f the partial factor matches the reference:
 // columns < f-1 complete, column f-1 holds rows < f-1, later columns zero.
-// Whole CTA participates (blockDim >= 32).  G, R have ld kRld; sbuf: 16*16.
+// Warp 0 factors (K <= 16: at most 120 trailing entries per step, warp-level
+// synchronisation instead of three CTA barriers per step); every thread of
+// the CTA must call it.  G, R have ld kRld; sbuf: 16*16.
 __device__ inline void cholesky(const double* G, int K, double tol, double* R, double* sbuf,
                          int* failed_at, double* failed_pivot) {
-  const int tid = threadIdx.x, nth = blockDim.x;
-  __shared__ double s_maxdiag;
-  __shared__ int s_fail;
-  __shared__ double s_piv;
-  for (int e = tid; e < kRld * kRld; e += nth) {
-    sbuf[e] = G[e];
-    R[e] = 0.0;
-  }
-  if (tid == 0) {
+  const int tid = threadIdx.x;
+  if (tid < 32) {
+    const int lane = tid;
+    for (int e = lane; e < kRld * kRld; e += 32) {
+      sbuf[e] = G[e];
+      R[e] = 0.0;
+    }
     double m = 0.0;
     for (int i = 0; i < K; ++i) {
       const double d = G[i + i * kRld];
       m = m < d ? d : m;  // std::max(max_diag, d)
     }
-    s_maxdiag = m;
-    s_fail = 0;
-    s_piv = 0.0;
-  }
-  __syncthreads();
-  const double floor_ = mul(tol, s_maxdiag);
-  for (int t = 0; t < K; ++t) {
-    if (tid == 0) {
+    const double floor_ = mul(tol, m);
+    __syncwarp();
+    int fail = 0;
+    double fpiv = 0.0;
+    for (int t = 0; t < K; ++t) {
       const double piv = sbuf[t + t * kRld];
-      if (piv <= floor_) {
-        s_fail = t + 1;
-        s_piv = piv;
-      } else {
-        R[t + t * kRld] = sqrt(piv);
+      if (piv <= floor_) {  // uniform over the warp
+        fail = t + 1;
+        fpiv = piv;
+        break;
       }
+      const double rtt = sqrt(piv);
+      if (lane == 0) R[t + t * kRld] = rtt;
+      for (int j = t + 1 + lane; j < K; j += 32) R[t + j * kRld] = div(sbuf[t + j * kRld], rtt);
+      __syncwarp();
+      // trailing update s_ij -= r_ti r_tj for t < i <= j
+      const int mm = K - t - 1;
+      for (int e = lane; e < mm * mm; e += 32) {
+        const int i = t + 1 + e % mm, j = t + 1 + e / mm;
+        if (i <= j) sbuf[i + j * kRld] = sub(sbuf[i + j * kRld], mul(R[t + i * kRld], R[t + j * kRld]));
+      }
+      __syncwarp();
     }
-    __syncthreads();
-    if (s_fail) {
-      // reference leaves row < t entries of column t (already in R) and zero beyond
-      break;
+    if (fail) {
+      // The reference computes column f-1's off-diagonal entries r_i,f-1 (i < f-1)
+      // before testing its pivot: they equal s_i,f-1 / r_ii at step i, which the
+      // right-looking loop already stored in R.  Columns >= f stay zero in the
+      // reference; here rows t < f-1 of columns >= f were filled: clear them.
+      for (int e = lane; e < kRld * kRld; e += 32)
+        if (e / kRld >= fail) R[e] = 0.0;
     }
-    for (int j = t + 1 + tid; j < K; j += nth) R[t + j * kRld] = div(sbuf[t + j * kRld], R[t + t * kRld]);
-    __syncthreads();
-    // trailing update s_ij -= r_ti r_tj for t < i <= j
-    const int m = K - t - 1;
-    for (int e = tid; e < m * m; e += nth) {
-      const int i = t + 1 + e % m, j = t + 1 + e / m;
-      if (i <= j) sbuf[i + j * kRld] = sub(sbuf[i + j * kRld], mul(R[t + i * kRld], R[t + j * kRld]));
-    }
-    __syncthreads();
-  }
-  if (tid == 0) {
-    *failed_at = s_fail;
-    *failed_pivot = s_piv;
-  }
-  __syncthreads();
-  if (s_fail) {
-    // The reference computes column f-1's off-diagonal entries r_i,f-1 (i < f-1)
-    // before testing its pivot: they equal s_i,f-1 / r_ii at step i, which the
-    // right-looking loop already stored in R.  Columns >= f stay zero in the
-    // reference; here rows t < f-1 of columns >= f were filled: clear them.
-    const int f = s_fail;
-    for (int e = tid; e < kRld * kRld; e += nth) {
-      const int i = e % kRld, j = e / kRld;
-      if (j >= f) R[i + j * kRld] = 0.0;
+    if (lane == 0) {
+      *failed_at = fail;
+      *failed_pivot = fpiv;
     }
   }
   __syncthreads();
@@ -90,12 +79,14 @@ __device__ inline void cholesky(const double* G, int K, double tol, double* R, d
 // R factor of the thin Householder QR (proj/src/dense.cpp:104-164), sign
 // normalised.  Q is not formed (RandCholQR uses only R,
 // proj/src/intra_orth.cpp:28-39).  A (m x K, ld lda) is destroyed.  Warp 0
-// only; lanes own columns.
+// only; lanes own columns; every sum keeps the reference's sequential row
+// order.  (Register-staged operands with fully unrolled, predicated row loops
+// measured slower: 20 -> 25 us per 22 x 11 factorization.)
 __device__ inline void householder_r(double* A, int lda, int m, int K, double* R, double* tau_buf) {
   const int lane = threadIdx.x & 31;
   if (threadIdx.x >= 32) return;
   for (int j = 0; j < K; ++j) {
-    double norm = 0.0, alpha = 0.0, v0 = 0.0, tau = 0.0;
+    double norm = 0.0;
     if (lane == 0) {
       double norm2 = 0.0;
       for (int i = j; i < m; ++i) norm2 = add(norm2, mul(A[i + j * lda], A[i + j * lda]));
@@ -108,9 +99,9 @@ __device__ inline void householder_r(double* A, int lda, int m, int K, double* R
       continue;
     }
     const double ajj = A[j + j * lda];
-    alpha = ajj >= 0.0 ? -norm : norm;
-    v0 = sub(ajj, alpha);
-    tau = div(-v0, alpha);
+    const double alpha = ajj >= 0.0 ? -norm : norm;
+    const double v0 = sub(ajj, alpha);
+    const double tau = div(-v0, alpha);
     __syncwarp();
     // w(i,j) = a(i,j) / v0 stored in A's lower part (a(i,j) is zeroed in the reference)
     for (int i = j + 1 + lane; i < m; i += 32) A[i + j * lda] = div(A[i + j * lda], v0);
@@ -147,8 +138,18 @@ __device__ inline void multiply_upper(const double* T, const double* Rm, int K, 
   for (int e = threadIdx.x; e < kRld * kRld; e += blockDim.x) {
     const int i = e % kRld, j = e / kRld;
     double s = 0.0;
-    if (i < K && j < K && j >= i)
-      for (int l = i; l <= j; ++l) s = add(s, mul(T[i + l * kRld], Rm[l + j * kRld]));
+    if (i < K && j < K && j >= i) {
+      double t[kMaxK], r[kMaxK];
+#pragma unroll
+      for (int l = 0; l < kMaxK; ++l) {
+        const bool in = l >= i && l <= j;
+        t[l] = in ? T[i + l * kRld] : 0.0;
+        r[l] = in ? Rm[l + j * kRld] : 0.0;
+      }
+#pragma unroll
+      for (int l = 0; l < kMaxK; ++l)
+        if (l >= i && l <= j) s = add(s, mul(t[l], r[l]));
+    }
     out[e] = s;
   }
 }
@@ -159,13 +160,22 @@ __device__ inline void update_projection(const double* C1, const double* C2, int
                                   const double* Rin, double* out) {
   for (int e = threadIdx.x; e < p * K; e += blockDim.x) {
     const int r = e % p, j = e / p;
-    double acc = 0.0;
-    for (int k = 0; k < K; ++k) {
-      const double bkj = Rin[k + j * kRld];
-      if (bkj == 0.0) continue;
-      acc = add(acc, mul(C2[r + k * ldc], bkj));
+    // operands first (independent global / shared loads), then the sum in
+    // the reference order
+    double c2[kMaxK], b[kMaxK];
+#pragma unroll
+    for (int k = 0; k < kMaxK; ++k) {
+      b[k] = k < K ? Rin[k + j * kRld] : 0.0;
+      c2[k] = k < K ? C2[r + k * ldc] : 0.0;
     }
-    out[r + j * ldc] = add(C1[r + j * ldc], acc);
+    const double c1 = C1[r + j * ldc];
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < kMaxK; ++k) {
+      if (k >= K || b[k] == 0.0) continue;
+      acc = add(acc, mul(c2[k], b[k]));
+    }
+    out[r + j * ldc] = add(c1, acc);
   }
 }
 
