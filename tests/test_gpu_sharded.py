@@ -77,15 +77,19 @@ def _worker(rank, world, port, case, out_dir):
             out = sk.apply(ctx.from_host(np.ascontiguousarray(v[rb:re_])), P.ReduceLedger())
             want = orc.sketch_apply(orc.sketch_build(code, n, 20, 5).h, v)
             res[f"wide_{kind}_rel"] = float(np.max(np.abs(out - want)) / np.max(np.abs(want)))
-    elif case in ("bcgs2_rand", "bcgs2_cholqr2"):
+    elif case in ("bcgs2_rand", "bcgs2_cholqr2", "bcgs2_count"):
+        # bcgs2_count: RandCholQR with a Count sketch (242 buckets at s = 10):
+        # its Householder block is 242 x 11, larger than the static scratch the
+        # unfused (multi-rank) finalize kernel had before it sized it by mh
         n, k, panels = 20_000, 11, 4
-        intra = 1 if case == "bcgs2_rand" else 0
+        intra = 0 if case == "bcgs2_cholqr2" else 1
+        kind, code = ("count", 1) if case == "bcgs2_count" else ("gaussian", 0)
         v = orc.gen_glued(n, panels, k, 1e6, 1e6, 7)
         ctx, rb, re_ = ctx_for(n)
-        th = P.SketchOperator.build(ctx, "gaussian", n, k - 1, 1) if intra else None
+        th = P.SketchOperator.build(ctx, kind, n, k - 1, 1) if intra else None
         st = P.BasisStore(ctx, panels * k)
         ob = orc.basis_new(n, panels * k)
-        oth = orc.sketch_build(0, n, k - 1, 1).h if intra else None
+        oth = orc.sketch_build(code, n, k - 1, 1).h if intra else None
         for p in range(panels):
             vp = v[:, p * k:(p + 1) * k]
             P.bcgs2(st, ctx.from_host(vp[rb:re_]), intra, th)
@@ -140,7 +144,7 @@ def test_sharded_sketches(gpu, tmp_path):
     assert r["wide_count_rel"] < 1e-13 and r["wide_countgauss_rel"] < 1e-13
 
 
-@pytest.mark.parametrize("case", ["bcgs2_rand", "bcgs2_cholqr2"])
+@pytest.mark.parametrize("case", ["bcgs2_rand", "bcgs2_cholqr2", "bcgs2_count"])
 def test_sharded_bcgs2(gpu, tmp_path, case):
     """sharded BCGS2: identical ledger, one physical all-reduce per ledger
     event, basis and R within the single-GPU tolerance"""
