@@ -231,14 +231,18 @@ int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st) {
   // Pre-solve passes (bo_pass.cuh SPLIT) consume a tile in two hand-offs
   // (solve warps, then the U/S/R group), so they want a deeper ring than
   // double buffering; BO_NS_PRE sets the stage count they try for first.
+  // A third stage helps only while the tile stays >= 128 rows (measured on the
+  // C2 sequence, scripts/ab_passes.sh: P2_QTX p = 11 419 -> 373 us, p <= 33
+  // P2_UPD_GRAM_ST -15 us; forcing 64-row tiles at p >= 44 lost 200 us each).
   static const int ns_pre = [] {
     const char* e = getenv("BO_NS_PRE");
-    return e ? std::max(2, atoi(e)) : 2;
+    return e ? std::max(2, atoi(e)) : 3;
   }();
   const int want_hi = (ki.npre > 0 && !rowg_kind) ? ns_pre : 2;
   for (int want_ns : {want_hi, 2, 1}) {
     for (int tt : {256, 128, 64}) {
       if (T) break;
+      if (want_ns > 2 && tt < 128 && !tile_env) continue;
       if (r.exact && tt != 64) continue;
       if (tile_env && tt != tile_env) continue;
       if (tt > tile_max) continue;
