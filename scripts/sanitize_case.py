@@ -1,7 +1,7 @@
 """Small workload for compute-sanitizer (memcheck / racecheck / synccheck):
 one config-1 GMRES restart for each one-stage scheme and the two-stage
 RandBCGS, a six-panel bcgs2 sequence (both intras, deferred), a Count-sketch
-sequence, and the matrix powers.  Exits non-zero on any library error.
+sequence, and the matrix powers (2-D 4-row kernel, 3-D plane-marching kernel).  Exits non-zero on any library error.
     compute-sanitizer --tool racecheck python scripts/sanitize_case.py"""
 import sys
 from pathlib import Path
@@ -35,5 +35,15 @@ for intra, sk in ((0, None), (1, "gaussian"), (1, "count")):
     print("bcgs2", intra, sk, "orth", float(np.linalg.norm(np.eye(6 * k) - q.T @ q, 2)))
 vk = ctx.to_host(op.mpk(ctx.from_host(np.random.default_rng(0).standard_normal(n)), 5))
 print("mpk", float(np.abs(vk).max()))
+# the plane-marching 3-D stencil kernel (bulk-copy plane ring, mbarriers):
+# 3-D Laplace and convection-diffusion, bit-exact against the CSR kernel
+n3 = 24 ** 3
+ctx3 = P.Context(n3)
+x3 = ctx3.from_host(np.random.default_rng(1).standard_normal(n3))
+for mk in (lambda c: P.Operator.laplace(c, 3, 24), lambda c: P.Operator.convdiff(c, 24)):
+    o3 = mk(ctx3)
+    y = ctx3.to_host(o3.mpk(x3, 5))
+    print("mpk 3-D", float(np.abs(y).max()))
+ctx3.synchronize()
 ctx.synchronize()
 print("sanitize case ok")
