@@ -58,6 +58,9 @@ def parse():
     ap.add_argument("--cpu-rows", type=int, default=1 << 18)
     ap.add_argument("--ref-cores", type=int, default=0, help="--impl reference: cap on host cores (0 = all usable)")
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu")
+    ap.add_argument("--panel-cache", default="",
+                    help="raw FP64 + SHA-256 cache of the C2 panels (bo_panel_cache_*): read and verified when "
+                         "the file exists, written from the device generator otherwise (one process)")
     ap.add_argument("--comm", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: collectives through torch.distributed gloo (bo_ctx_create_comm), every rank on "
                          "cuda:LOCAL_RANK %% device_count - exercises the multi-rank bench on one GPU")
@@ -252,12 +255,30 @@ def run_reference_arm(args):
 
 
 # --------------------------------------------------------------------- ours --
+INPUT = {}  # where the C2 panels came from (printed in the config)
+
+
 def make_panels(P, ctx, args):
     """The C2 input: gen_glued(n, panels, k, kappa, kappa, 7) (problems.cpp:21-61)
     from the device generator, bit-identical to the reference's
-    (tests/test_gpu_c2_full.py pins it by sha256); each rank keeps its rows."""
+    (tests/test_gpu_c2_full.py pins it by sha256); each rank keeps its rows.
+    With --panel-cache the panels come from / go to a raw FP64 + SHA-256 file
+    (SURVEY.md §8(d) C2), so separate runs consume identical, verified bytes."""
     k = args.s + 1
-    v = P.gen_glued(ctx, args.panels, k, args.kappa, args.kappa, 7)
+    desc = f"gen_glued({args.n}, {args.panels}, {k}, {args.kappa:g}, {args.kappa:g}, 7)"
+    if args.panel_cache and ctx.n_local == args.n:
+        path = Path(args.panel_cache)
+        if path.exists() and P.borth.panel_cache_info(path)["desc"] == desc:
+            host = P.borth.panel_cache_read(path)  # raises on a digest mismatch
+            v = ctx.from_host(host)
+            INPUT.update(source="panel cache", path=str(path), sha256=P.borth.panel_cache_info(path)["sha256"])
+        else:
+            v = P.gen_glued(ctx, args.panels, k, args.kappa, args.kappa, 7)
+            sha = P.borth.panel_cache_write(path, ctx.to_host(v), desc)
+            INPUT.update(source="device gen_glued, cached", path=str(path), sha256=sha)
+    else:
+        v = P.gen_glued(ctx, args.panels, k, args.kappa, args.kappa, 7)
+        INPUT.update(source="device gen_glued (bit-identical to the reference's)")
     return [v[p * k:(p + 1) * k] for p in range(args.panels)]
 
 
@@ -617,7 +638,7 @@ def main():
             "vs_baseline": None, "dtype": "f64",
             "data": f"synthetic: reference gen_glued panels (device generator, bit-identical; "
                     f"{t_gen:.1f} s setup), Gaussian sketch seed 1",
-            "config": workload_config(args, world),
+            "config": dict(workload_config(args, world), input=INPUT),
             "c2_parity": c2_parity,
             "roofline": {"bound": "hbm", "kernel": f"pass_kernel {top_kind} (p={top_p})", "achieved": achieved,
                          "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,

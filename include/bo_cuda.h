@@ -281,6 +281,18 @@ int bo_csr_host_arrays(bo_csr_host h, int64_t* row_ptr, int64_t* col, double* va
 int bo_csr_host_destroy(bo_csr_host h);
 int bo_mm_write(const char* path, uint64_t nrows, uint64_t ncols, const int64_t* row_ptr, const int64_t* col,
                 const double* val, bo_status* st);
+/* Raw FP64 panel cache for C2 inputs: a
+ * 312-byte header (magic "BOPC0001", rows, cols, SHA-256 of the payload, a
+ * 256-byte generator description) followed by rows x cols doubles,
+ * column-major.  Write hashes the host block (ld >= rows) and writes through a
+ * temporary file; read fills a host block and fails with BO_INVALID on a size
+ * or digest mismatch.  Host only.  bo_sha256: the same digest of any buffer. */
+int bo_panel_cache_write(const char* path, const double* a, uint64_t rows, uint64_t cols, uint64_t ld,
+                         const char* desc, char sha_hex[65], bo_status* st);
+int bo_panel_cache_info(const char* path, uint64_t* rows, uint64_t* cols, char sha_hex[65], char desc[256],
+                        bo_status* st);
+int bo_panel_cache_read(const char* path, double* a, uint64_t rows, uint64_t cols, uint64_t ld, bo_status* st);
+int bo_sha256(const void* data, uint64_t len, char hex_out[65]);
 /* Cost model (cost_model.hpp:9-39, cost_model.cpp:38-111): exact integer
  * per-restart-cycle flops (both orthogonalization passes), latency (global
  * reduces), volume and storage of the tabulated schemes.  shat is forced to

@@ -16,7 +16,8 @@ CSRC = PKG / "csrc"
 LIB = PKG / "libbo_cuda.so"
 INCLUDE = PKG.parent / "include"
 
-SOURCES = ["bo_capi.cu", "bo_ops.cu", "bo_gmres.cu", "bo_glued.cu", "mt64_jump.cpp", "bo_io.cpp", "bo_cost.cpp"]
+SOURCES = ["bo_capi.cu", "bo_ops.cu", "bo_gmres.cu", "bo_glued.cu", "mt64_jump.cpp", "bo_io.cpp", "bo_cost.cpp",
+           "bo_cache.cpp"]
 # the pass-engine instantiation units: bo_pass_inst.cu compiled once per combination
 INST_UNITS = [f"-DBO_INST_NT={nt} -DBO_INST_T={t}" for nt in (1, 2) for t in (256, 128, 64)] + \
              [f"-DBO_INST_KC={kc} -DBO_INST_T={t}" for kc in (6, 11, 13, 16) for t in (256, 128, 64)] + ["-DBO_INST_EXACT"]

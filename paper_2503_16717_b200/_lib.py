@@ -145,6 +145,10 @@ _SIGS = {
     "bo_mpk": (C.c_int, [vp, vp, u64, vp, u64, SP]),
     "bo_sstep_gmres": (C.c_int, [vp, vp, vp, C.POINTER(SolverConfig), vp, C.POINTER(SolveReport), SP]),
     "bo_mt64_jump_window": (C.c_int, [u64, u64, u64p]),
+    "bo_panel_cache_write": (C.c_int, [C.c_char_p, dp, u64, u64, u64, C.c_char_p, C.c_char_p, SP]),
+    "bo_panel_cache_info": (C.c_int, [C.c_char_p, u64p, u64p, C.c_char_p, C.c_char_p, SP]),
+    "bo_panel_cache_read": (C.c_int, [C.c_char_p, dp, u64, u64, u64, SP]),
+    "bo_sha256": (C.c_int, [C.c_void_p, u64, C.c_char_p]),
 }
 
 _lib = None

@@ -728,6 +728,46 @@ def write_matrix_market(path, nrows: int, ncols: int, row_ptr, col, val):
           ci.ctypes.data_as(C.POINTER(C.c_int64)), _dp(vv))
 
 
+# ------------------------------------------------------ C2 panel cache --
+def panel_cache_write(path, a: np.ndarray, desc: str = "") -> str:
+    """Raw FP64 panel cache (bo_panel_cache_write): a column-major host block
+    (rows x cols) with its SHA-256 in the header; returns the hex digest."""
+    lib = L.load()
+    a = np.asfortranarray(a, dtype=np.float64)
+    sha = C.create_string_buffer(65)
+    _call(lib.bo_panel_cache_write, str(path).encode(), _dp(a), a.shape[0], a.shape[1], a.shape[0],
+          desc.encode(), sha)
+    return sha.value.decode()
+
+
+def panel_cache_info(path) -> dict:
+    lib = L.load()
+    rows, cols = C.c_uint64(), C.c_uint64()
+    sha, desc = C.create_string_buffer(65), C.create_string_buffer(257)
+    _call(lib.bo_panel_cache_info, str(path).encode(), C.byref(rows), C.byref(cols), sha, desc)
+    return {"rows": rows.value, "cols": cols.value, "sha256": sha.value.decode(), "desc": desc.value.decode()}
+
+
+def panel_cache_read(path, out: np.ndarray | None = None) -> np.ndarray:
+    """read a panel cache into a column-major host array, verifying the digest
+    (raises Error on a size or SHA-256 mismatch)"""
+    lib = L.load()
+    info = panel_cache_info(path)
+    if out is None:
+        out = np.empty((info["rows"], info["cols"]), order="F")
+    _call(lib.bo_panel_cache_read, str(path).encode(), _dp(out), out.shape[0], out.shape[1], out.shape[0])
+    return out
+
+
+def sha256(a: np.ndarray) -> str:
+    """SHA-256 of an array's bytes in memory order (bo_sha256)"""
+    lib = L.load()
+    a = np.ascontiguousarray(a) if not a.flags.f_contiguous else a
+    out = C.create_string_buffer(65)
+    lib.bo_sha256(a.ctypes.data_as(C.c_void_p), a.nbytes, out)
+    return out.value.decode()
+
+
 def gen_glued(ctx: Context, num_panels: int, panel_width: int, kappa_panel: float, kappa_global: float,
               seed: int):
     """gen_glued (problems.cpp:21-61) over the context's n global rows,

@@ -233,3 +233,44 @@ def test_cost_model_matches_reference(ref):
                             checked += 1
     assert checked > 10000
     assert P.eval_cost("sstep", 8_000_000, 60, 10)["latency"] == 24
+
+
+# ------------------------------------------------------- C2 panel cache --
+def test_sha256_matches_hashlib():
+    import hashlib
+
+    import paper_2503_16717_b200 as P
+    rng = np.random.default_rng(3)
+    for n in (0, 1, 55, 56, 63, 64, 65, 119, 1000, 1 << 20):
+        b = rng.integers(0, 256, n, dtype=np.uint8)
+        assert P.borth.sha256(b) == hashlib.sha256(b.tobytes()).hexdigest(), n
+
+
+def test_panel_cache_roundtrip_and_digest(tmp_path):
+    """raw FP64 + SHA-256; the digest is that of
+    the column-major payload, reading verifies it, corruption and shape
+    mismatches fail loudly"""
+    import hashlib
+
+    import paper_2503_16717_b200 as P
+    rng = np.random.default_rng(4)
+    a = np.asfortranarray(rng.standard_normal((1003, 22)))
+    path = tmp_path / "c2.bopc"
+    sha = P.borth.panel_cache_write(path, a, "gen_glued(1003, 2, 11, 100, 100, 7)")
+    assert sha == hashlib.sha256(a.tobytes(order="F")).hexdigest()
+    info = P.borth.panel_cache_info(path)
+    assert info == {"rows": 1003, "cols": 22, "sha256": sha, "desc": "gen_glued(1003, 2, 11, 100, 100, 7)"}
+    b = P.borth.panel_cache_read(path)
+    assert np.array_equal(a, b) and b.flags.f_contiguous
+    raw = bytearray(path.read_bytes())
+    raw[312 + 8 * 500] ^= 1  # one payload bit
+    bad = tmp_path / "bad.bopc"
+    bad.write_bytes(bytes(raw))
+    with pytest.raises(P.borth.Error, match="SHA-256 mismatch"):
+        P.borth.panel_cache_read(bad)
+    with pytest.raises(P.borth.Error, match="holds 1003 x 22"):
+        P.borth.panel_cache_read(path, np.empty((1003, 11), order="F"))
+    bad.write_bytes(b"X" * 400)
+    with pytest.raises(P.borth.Error, match="bad magic"):
+        P.borth.panel_cache_info(bad)
+    assert not (tmp_path / "c2.bopc.tmp").exists()  # written through a temporary, renamed at the end
