@@ -265,9 +265,10 @@ def make_panels(P, ctx, args):
     With --panel-cache the panels come from / go to a raw FP64 + SHA-256 file
     (SURVEY.md §8(d) C2), so separate runs consume identical, verified bytes."""
     k = args.s + 1
-    desc = f"gen_glued({args.n}, {args.panels}, {k}, {args.kappa:g}, {args.kappa:g}, 7)"
-    if args.panel_cache and ctx.n_local == args.n:
-        path = Path(args.panel_cache)
+    n, cache = ctx.n_global, getattr(args, "panel_cache", "")
+    desc = f"gen_glued({n}, {args.panels}, {k}, {args.kappa:g}, {args.kappa:g}, 7)"
+    if cache and ctx.n_local == n:
+        path = Path(cache)
         if path.exists() and P.borth.panel_cache_info(path)["desc"] == desc:
             host = P.borth.panel_cache_read(path)  # raises on a digest mismatch
             v = ctx.from_host(host)

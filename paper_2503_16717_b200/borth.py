@@ -283,6 +283,7 @@ class Context:
             _call(self.lib.bo_ctx_create, device, rank, world, idbuf, n, row_begin, row_end,
                   C.c_void_p(self.stream.cuda_stream), C.byref(h))
         self.h = h
+        self.n_global = int(n)
         self.n_local = int(self.lib.bo_ctx_local_rows(h))
         self.ld = int(self.lib.bo_ctx_ld(h))
         self._children = weakref.WeakSet()
