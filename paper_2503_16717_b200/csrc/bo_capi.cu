@@ -462,10 +462,11 @@ int comm_allgather_u64(bo_ctx ctx, const uint64_t* send, size_t n, uint64_t* rec
   const int rc = nc.AllGather(send, recv, n, kNcclUint64, ctx->nccl, ctx->stream);
   return rc ? set_st(st, BO_NCCL, rc, 0.0, "ncclAllGather failed (%d)", rc) : BO_OK;
 }
-int comm_exchange(bo_ctx ctx, int nops, const bo_p2p_op* ops, bo_status* st) {
+int comm_exchange(bo_ctx ctx, int nops, const bo_p2p_op* ops, bo_status* st, cudaStream_t s) {
   if (nops == 0) return BO_OK;
+  if (!s) s = ctx->stream;
   if (ctx->has_comm) {
-    const int rc = ctx->comm.exchange_f64(ctx->comm.user, nops, ops, ctx->stream);
+    const int rc = ctx->comm.exchange_f64(ctx->comm.user, nops, ops, s);
     return rc ? set_st(st, BO_NCCL, rc, 0.0, "exchange callback failed (%d)", rc) : BO_OK;
   }
   NcclApi& nc = nccl();
@@ -473,9 +474,9 @@ int comm_exchange(bo_ctx ctx, int nops, const bo_p2p_op* ops, bo_status* st) {
   nc.GroupStart();
   for (int i = 0; i < nops; ++i) {
     if (ops[i].is_send)
-      nc.Send(ops[i].buf, ops[i].count, kNcclFloat64, ops[i].peer, ctx->nccl, ctx->stream);
+      nc.Send(ops[i].buf, ops[i].count, kNcclFloat64, ops[i].peer, ctx->nccl, s);
     else
-      nc.Recv(ops[i].buf, ops[i].count, kNcclFloat64, ops[i].peer, ctx->nccl, ctx->stream);
+      nc.Recv(ops[i].buf, ops[i].count, kNcclFloat64, ops[i].peer, ctx->nccl, s);
   }
   const int rc = nc.GroupEnd();
   return rc ? set_st(st, BO_NCCL, rc, 0.0, "NCCL group send/recv failed (%d)", rc) : BO_OK;
@@ -654,6 +655,9 @@ extern "C" int bo_ctx_destroy(bo_ctx c) {
   cudaFree(c->spare_buf);
   cudaFree(c->gen_plan.dev);
   if (c->own_stream) cudaStreamDestroy(c->stream);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->ev_x) cudaEventDestroy(c->ev_x);
+  if (c->ev_halo) cudaEventDestroy(c->ev_halo);
   delete c;
   return BO_OK;
 }

@@ -15,6 +15,10 @@ struct bo_ctx_s {
   int rank = 0, world = 1;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  // halo exchanges of a sharded SpMV run here, overlapped with the interior
+  // planes on `stream` (created lazily; ev_x: x ready, ev_halo: halos landed)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_x = nullptr, ev_halo = nullptr;
   void* nccl = nullptr;  // ncclComm_t
   bool has_comm = false;  // collectives through host callbacks (bo_ctx_create_comm)
   bo_comm_ops comm{};
@@ -277,7 +281,7 @@ int comm_allreduce(bo_ctx ctx, double* buf, size_t n, bo_status* st);
 void prefetch_theta_g(uint64_t seed, uint64_t mc, uint64_t mhat);
 std::vector<double> take_theta_g(uint64_t seed, uint64_t mc, uint64_t mhat);
 int comm_allgather_u64(bo_ctx ctx, const uint64_t* send, size_t n, uint64_t* recv, bo_status* st);
-int comm_exchange(bo_ctx ctx, int nops, const bo_p2p_op* ops, bo_status* st);
+int comm_exchange(bo_ctx ctx, int nops, const bo_p2p_op* ops, bo_status* st, cudaStream_t s = nullptr);
 int op_apply(bo_op op, const double* x, double* y, bo_status* st);
 int sketch_to_host(bo_sketch th, const double* v, uint64_t ldv, int K, std::vector<double>& S, bo_status* st);
 inline uint64_t round_up(uint64_t x, uint64_t m) { return (x + m - 1) / m * m; }

@@ -272,6 +272,7 @@ __global__ void __launch_bounds__(256, BO_SPMV_MINB) spmv_stencil4_halo_kernel(i
 constexpr int kMarchRing = 4;
 template <int PT>
 __global__ void __launch_bounds__(512) spmv_stencil7_march_kernel(uint32_t k, uint32_t jb, uint32_t ip0, uint32_t np,
+                                                                  uint32_t qlo, uint32_t qhi,
                                                                   const Stencil st, const double* __restrict__ x,
                                                                   const double* __restrict__ hlo,
                                                                   const double* __restrict__ hhi,
@@ -284,7 +285,8 @@ __global__ void __launch_bounds__(512) spmv_stencil7_march_kernel(uint32_t k, ui
   // the (line block, plane) steps are split into equal contiguous ranges, one
   // per CTA (a persistent grid): every SM gets the same work; a range that
   // crosses into the next line block restarts the march there
-  const uint64_t total = (uint64_t)nbj * np;
+  const uint32_t nq = qhi - qlo;  // planes [qlo, qhi) of the shard (all, the interior or one boundary plane)
+  const uint64_t total = (uint64_t)nbj * nq;
   const uint64_t u0 = total * blockIdx.x / gridDim.x, u1 = total * (blockIdx.x + 1) / gridDim.x;
   auto plane = [&](int q) -> const double* { return q < 0 ? hlo : (q >= (int)np ? hhi : x + (size_t)q * kk); };
   // plane q (local) exists if its global index is in [0, k) and q in [-1, np]
@@ -305,9 +307,9 @@ __global__ void __launch_bounds__(512) spmv_stencil7_march_kernel(uint32_t k, ui
   const double c_ilo = st.c[0], c_jlo = st.c[1], c_llo = st.c[2], c_self = st.c[3];
   const double c_lhi = st.c[4], c_jhi = st.c[5], c_ihi = st.c[6];
   for (uint64_t u = u0; u < u1;) {
-    const uint32_t jbk = (uint32_t)(u / np), q0 = (uint32_t)(u % np);
+    const uint32_t jbk = (uint32_t)(u / nq), q0 = qlo + (uint32_t)(u % nq);
     const uint64_t qe = q0 + (u1 - u);
-    const uint32_t q1 = qe < np ? (uint32_t)qe : np;
+    const uint32_t q1 = qe < qhi ? (uint32_t)qe : qhi;
     u += q1 - q0;
     const uint32_t j0 = jbk * jb, j = j0 + ty;
     const bool act = ty < jb && j < k;
@@ -800,7 +802,8 @@ int op_setup_halo(bo_op op, long long need_lo, long long need_hi, bo_status* st)
 // Fills the halo rows of op->xext from the neighbour ranks.  copy_local also
 // copies the local rows into its middle, for kernels that index x as one
 // array (CSR columns); the 4-row stencil kernel reads x in place.
-int halo_exchange(bo_op op, const double* x, const double** xe, bool copy_local, bo_status* st) {
+int halo_exchange(bo_op op, const double* x, const double** xe, bool copy_local, bo_status* st,
+                  cudaStream_t s = nullptr) {
   bo_ctx ctx = op->ctx;
   if (!op->xext) {
     *xe = x;
@@ -821,7 +824,7 @@ int halo_exchange(bo_op op, const double* x, const double** xe, bool copy_local,
       if (op->halo_hi) ops[n++] = {r + 1, 0, op->xext + op->halo_lo + ctx->n_local, op->halo_hi};
       if (op->peer_need_lo) ops[n++] = {r + 1, 1, xs + ctx->n_local - op->peer_need_lo, op->peer_need_lo};
     }
-    TRY(comm_exchange(ctx, n, ops, st));
+    TRY(comm_exchange(ctx, n, ops, st, s));
   }
   *xe = op->xext;
   return BO_OK;
@@ -949,52 +952,86 @@ int op_apply(bo_op op, const double* x, double* y, bo_status* st) {
                    ctx->row_begin % 4 == 0 && nl % 4 == 0 && op->halo_lo % 4 == 0 && op->halo_hi % 4 == 0 &&
                    ((uintptr_t)x % 32) == 0 && ((uintptr_t)y % 32) == 0 &&
                    ((uintptr_t)(op->xext ? op->xext : x) % 32) == 0;
+  // plane-marching 3-D kernel: whole planes per shard, halos of one plane
+  static const bool march_on = [] {
+    const char* e = getenv("BO_SPMV_MARCH");
+    return !(e && atoi(e) == 0);
+  }();
+  const uint64_t kk = op->k * op->k;
+  const bool march = march_on && st4 && op->dims == 3 && op->k <= 512 && ctx->row_begin % kk == 0 &&
+                     nl % (long long)kk == 0 && (op->halo_lo == 0 || op->halo_lo == kk) &&
+                     (op->halo_hi == 0 || op->halo_hi == kk);
+  Stencil stc;
+  for (int q = 0; q < 7; ++q) stc.c[q] = op->coef[q];
+  if (march) {
+    // four points per thread, 256 threads (k = 200: five lines per CTA, four
+    // CTAs per SM).  Measured at n = 8e6 (scripts/prof_spmv.py): 30.7 us per
+    // SpMV; eight points per thread (BO_SPMV_PT=8, ten lines: fewer halo
+    // reads) 36.7 us, 384 / 512-thread CTAs 31.2 / 32.5 us, the 4-row
+    // kernel below 38 us.
+    static const int pt_env = [] {
+      const char* e = getenv("BO_SPMV_PT");
+      return e ? atoi(e) : 0;
+    }();
+    static const int tpb_env = [] {
+      const char* e = getenv("BO_SPMV_TPB");
+      return e ? atoi(e) : 256;
+    }();
+    static const bool overlap_on = [] {
+      const char* e = getenv("BO_HALO_OVERLAP");
+      return !(e && atoi(e) == 0);
+    }();
+    const uint32_t k = (uint32_t)op->k;
+    const uint32_t PT = (pt_env == 8 && k % 8 == 0 && k >= 64) ? 8 : 4, G = k / PT;
+    const uint32_t jb = std::max<uint32_t>(1, std::min<uint32_t>((uint32_t)std::min(512, tpb_env) / G, k));
+    const uint32_t nbj = (k + jb - 1) / jb, np = (uint32_t)(nl / (long long)kk);
+    const size_t smem = (size_t)kMarchRing * (jb + 2) * k * 8;
+    const uint32_t per_sm = (uint32_t)std::max<size_t>(1, std::min<size_t>(4, (220 * 1024) / smem));
+    const double* hlo = op->xext ? op->xext + op->halo_lo - kk : x;  // the plane below (when it exists)
+    const double* hhi = op->xext ? op->xext + op->halo_lo + nl : x;
+    auto kfn = PT == 8 ? spmv_stencil7_march_kernel<8> : spmv_stencil7_march_kernel<4>;
+    if (smem > 48 * 1024)
+      CU(cudaFuncSetAttribute((const void*)kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // persistent grid over planes [qlo, qhi): as many CTAs as fit on the SMs at once, equal shares
+    auto launch = [&](uint32_t qlo, uint32_t qhi) {
+      const uint32_t grid_m =
+          std::max<uint32_t>(1, std::min<uint32_t>(nbj * (qhi - qlo), (uint32_t)ctx->num_sms * per_sm));
+      kfn<<<grid_m, G * jb, smem, ctx->stream>>>(k, jb, (uint32_t)(ctx->row_begin / kk), np, qlo, qhi, stc, x, hlo,
+                                                  hhi, y);
+      ctx->launches++;
+    };
+    const double* xe;
+    if (op->xext && ctx->world > 1 && np >= 3 && overlap_on) {
+      // Sharded: the interior planes 1 .. np-2 read only local planes, so they
+      // run while the halo planes travel on a side stream (NCCL p2p or the
+      // host transport); the two boundary planes follow the exchange.
+      if (!ctx->side) {
+        CU(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+        CU(cudaEventCreateWithFlags(&ctx->ev_x, cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&ctx->ev_halo, cudaEventDisableTiming));
+      }
+      CU(cudaEventRecord(ctx->ev_x, ctx->stream));  // x is ready
+      launch(1, np - 1);
+      CU(cudaStreamWaitEvent(ctx->side, ctx->ev_x, 0));
+      TRY(halo_exchange(op, x, &xe, false, st, ctx->side));
+      CU(cudaEventRecord(ctx->ev_halo, ctx->side));
+      CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_halo, 0));
+      launch(0, 1);
+      launch(np - 1, np);
+    } else {
+      TRY(halo_exchange(op, x, &xe, false, st));
+      launch(0, np);
+    }
+    CU(cudaGetLastError());
+    return BO_OK;
+  }
   const double* xe;
   TRY(halo_exchange(op, x, &xe, !st4, st));
   const int grid = (int)std::max<long long>(1, std::min<long long>((long long)ctx->num_sms * 8, (nl + 255) / 256));
   if (op->kind == 0)
     spmv_csr_kernel<<<grid, 256, 0, ctx->stream>>>(nl, op->row_ptr, op->col, op->val, xe, y);
   else {
-    Stencil stc;
-    for (int q = 0; q < 7; ++q) stc.c[q] = op->coef[q];
-    // plane-marching 3-D kernel: whole planes per shard, halos of one plane
-    static const bool march_on = [] {
-      const char* e = getenv("BO_SPMV_MARCH");
-      return !(e && atoi(e) == 0);
-    }();
-    const uint64_t kk = op->k * op->k;
-    const bool march = march_on && st4 && op->dims == 3 && op->k <= 512 && ctx->row_begin % kk == 0 &&
-                       nl % (long long)kk == 0 && (op->halo_lo == 0 || op->halo_lo == kk) &&
-                       (op->halo_hi == 0 || op->halo_hi == kk);
-    if (march) {
-      // four points per thread, 256 threads (k = 200: five lines per CTA, four
-      // CTAs per SM).  Measured at n = 8e6 (scripts/prof_spmv.py): 30.7 us per
-      // SpMV; eight points per thread (BO_SPMV_PT=8, ten lines: fewer halo
-      // reads) 36.7 us, 384 / 512-thread CTAs 31.2 / 32.5 us, the 4-row
-      // kernel below 38 us.
-      static const int pt_env = [] {
-        const char* e = getenv("BO_SPMV_PT");
-        return e ? atoi(e) : 0;
-      }();
-      const uint32_t k = (uint32_t)op->k;
-      static const int tpb_env = [] {
-        const char* e = getenv("BO_SPMV_TPB");
-        return e ? atoi(e) : 256;
-      }();
-      const uint32_t PT = (pt_env == 8 && k % 8 == 0 && k >= 64) ? 8 : 4, G = k / PT;
-      const uint32_t jb = std::max<uint32_t>(1, std::min<uint32_t>((uint32_t)std::min(512, tpb_env) / G, k));
-      const uint32_t nbj = (k + jb - 1) / jb, np = (uint32_t)(nl / (long long)kk);
-      const size_t smem = (size_t)kMarchRing * (jb + 2) * k * 8;
-      // persistent grid: as many CTAs as fit on the SMs at once, equal shares
-      const uint32_t per_sm = (uint32_t)std::max<size_t>(1, std::min<size_t>(4, (220 * 1024) / smem));
-      const uint32_t grid_m = std::max<uint32_t>(1, std::min<uint32_t>(nbj * np, (uint32_t)ctx->num_sms * per_sm));
-      const double* hlo = op->xext ? op->xext + op->halo_lo - kk : x;  // the plane below (when it exists)
-      const double* hhi = op->xext ? op->xext + op->halo_lo + nl : x;
-      auto kfn = PT == 8 ? spmv_stencil7_march_kernel<8> : spmv_stencil7_march_kernel<4>;
-      if (smem > 48 * 1024)
-        CU(cudaFuncSetAttribute((const void*)kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      kfn<<<grid_m, G * jb, smem, ctx->stream>>>(k, jb, (uint32_t)(ctx->row_begin / kk), np, stc, x, hlo, hhi, y);
-    } else if (st4) {
+    if (st4) {
       const uint32_t ng = (uint32_t)(nl / 4);
       // one 4-row group per thread, no grid-stride loop: as many loads in
       // flight as the SMs hold (ncu: the capped grid was latency-bound)
