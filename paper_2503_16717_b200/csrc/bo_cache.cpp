@@ -218,12 +218,12 @@ extern "C" int bo_panel_cache_read(const char* path, double* a, uint64_t rows, u
                                   std::to_string(cols));
   Sha256 s;
   bool good = rc == BO_OK;
-  for_each_column(a, rows, cols, ld, [&](const double* c, size_t bytes) {
-    if (!good) return;
-    double* dst = const_cast<double*>(c);
+  for (uint64_t c = 0; good && c < cols; ++c) {
+    double* dst = a + c * ld;
+    const size_t bytes = rows * sizeof(double);
     good = std::fread(dst, 1, bytes, f) == bytes;
     if (good) s.update(dst, bytes);
-  });
+  }
   std::fclose(f);
   if (rc != BO_OK) return rc;
   if (!good) return fail(st, BO_INVALID, std::string("panel cache: truncated payload in ") + path);
