@@ -61,8 +61,9 @@ __device__ __forceinline__ uint64_t mt_f(uint64_t hi_src, uint64_t lo_src) {
 //     windows are combined through shared memory.
 //  2. Generate.  Warps 27..31 (160 threads, one word each per half) twist
 //     window after window into a ring of kRing shared-memory windows
-//     (std::mt19937_64 order: two dependent halves per window, separated by
-//     a named barrier), while warps 0..24, in 5 groups of 5, temper and
+//     (std::mt19937_64 order; each lane writes word t and word t + 156,
+//     lane 155 recomputing new word 0, so one named barrier per window),
+//     while warps 0..24, in 5 groups of 5, temper and
 //     transform the 156 draw pairs of every 5th window (Box-Muller in FP64, or
 //     the Count bucket/sign) and store them.  Full/empty mbarriers hand the
 //     ring slots over; the FP64 transform is the bound.
@@ -159,18 +160,15 @@ __global__ void __launch_bounds__(1024, 1) mt_stream_kernel(const GenArgs a) {
       if (w >= kRing) ptx::mbar_wait(&empty[slot], (uint32_t)((w / kRing - 1) & 1));
       const uint64_t* cur = ring + ((w - 1) % kRing) * kMtN;
       uint64_t* nxt = ring + slot * kMtN;
-      uint64_t a0 = 0, a1 = 0;
       if (pt < kMtM) {
-        a0 = cur[pt];
-        a1 = cur[pt + 1];
-        nxt[pt] = cur[pt + kMtM] ^ mt_f(a0, a1);
-        a0 = cur[pt + kMtM];
-        a1 = pt + kMtM + 1 < kMtN ? cur[pt + kMtM + 1] : 0;
-      }
-      ptx::named_bar_sync(1, kGenProducerWarps * 32);
-      if (pt < kMtM) {
-        const int i = pt + kMtM;
-        nxt[i] = nxt[pt] ^ mt_f(a0, i + 1 < kMtN ? a1 : nxt[0]);
+        // word pt of the new window (mt19937_64 first half), then word
+        // pt + 156, which needs new word pt (this lane's) and, for the last
+        // word, new word 0: lane 155 recomputes it from the old window, so
+        // one barrier per window suffices (the next window reads this one)
+        const uint64_t lo = cur[pt + kMtM] ^ mt_f(cur[pt], cur[pt + 1]);
+        nxt[pt] = lo;
+        const uint64_t nx = pt + 1 < kMtM ? cur[pt + kMtM + 1] : (cur[kMtM] ^ mt_f(cur[0], cur[1]));
+        nxt[pt + kMtM] = lo ^ mt_f(cur[pt + kMtM], nx);
       }
       ptx::named_bar_sync(1, kGenProducerWarps * 32);
       if (pt == 0) ptx::mbar_arrive(&full[slot]);
