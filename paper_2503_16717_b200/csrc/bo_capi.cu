@@ -79,7 +79,7 @@ NcclApi& nccl() {
       }
     if (!api.h) return;
     api.GetUniqueId = (int (*)(void*))dlsym(api.h, "ncclGetUniqueId");
-    api.CommInitRank = (int (*)(void**, int, char*, int))dlsym(api.h, "ncclCommInitRank");
+    api.CommInitRank = (int (*)(void**, int, NcclUniqueId, int))dlsym(api.h, "ncclCommInitRank");
     api.AllReduce = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(
         api.h, "ncclAllReduce");
     api.CommDestroy = (int (*)(void*))dlsym(api.h, "ncclCommDestroy");
@@ -334,7 +334,7 @@ int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st) {
   if (f.ldc == 0) f.ldc = LDC;
   a.fin = f;
   static const bool unfuse = getenv("BO_UNFUSE_FIN") != nullptr;  // diagnostics: finalize as its own kernel
-  a.fused_finalize = (ctx->world == 1 && !unfuse) ? 1 : 0;
+  a.fused_finalize = (!ctx->collective && !unfuse) ? 1 : 0;
 
   PassFn fn = get_pass_fn(nt, T, r.kind, r.exact, r.K);
   static std::mutex mu;
@@ -380,7 +380,7 @@ int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st) {
   }
   if (!a.fused_finalize) {
     // one all-reduce per pass that reduces (a ledger event); store-only passes have none
-    if (ctx->world > 1 && (ki.qtx || ki.gram || ki.sk != SK_NONE))
+    if (ctx->collective && (ki.qtx || ki.gram || ki.sk != SK_NONE))
       TRY(comm_allreduce(ctx, ctx->sums, (size_t)a.part_len, st));
     if (f.ops) {
       const size_t fsm = (1536 + (size_t)std::max(f.mh, 32) * 16 + 64) * 8;
@@ -621,19 +621,21 @@ static int ctx_create_impl(int device, int rank, int world, const void* nccl_id,
   if (comm) {
     c->has_comm = true;
     c->comm = *comm;
-  } else if (world > 1) {
+    c->collective = world > 1;
+  } else if (world > 1 || nccl_id) {  // an id with world = 1: a size-1 communicator
     NcclApi& nc = nccl();
     if (!nc.ok) {
       bo_ctx_destroy(c);
       return set_st(st, BO_NCCL, 0, 0.0, "NCCL library not available");
     }
-    char id[128];
-    std::memcpy(id, nccl_id, 128);
+    NcclUniqueId id;
+    std::memcpy(id.internal, nccl_id, sizeof id.internal);
     int rc = nc.CommInitRank(&c->nccl, world, id, rank);
     if (rc) {
       bo_ctx_destroy(c);
       return set_st(st, BO_NCCL, 0, 0.0, "ncclCommInitRank failed (%d)", rc);
     }
+    c->collective = true;
   }
   *out = c;
   return BO_OK;

@@ -236,7 +236,7 @@ int reduce_sum(Gm& g, int nparts, double* out, bo_status* st) {
   CU(cudaStreamSynchronize(ctx->stream));
   double s = 0.0;
   for (int i = 0; i < nparts; ++i) s += g.hpart[i];
-  if (ctx->world > 1) {
+  if (ctx->collective) {
     CU(cudaMemcpyAsync(g.gsum, &s, 8, cudaMemcpyHostToDevice, ctx->stream));
     TRY(comm_allreduce(ctx, g.gsum, 1, st));
     CU(cudaMemcpyAsync(&s, g.gsum, 8, cudaMemcpyDeviceToHost, ctx->stream));
@@ -295,10 +295,10 @@ int cgs2_cycle(Gm& g, double* Q, uint64_t ld, const double* q1, uint64_t m, doub
   q_in = m;
   happy = false;
   auto finish = [&](double* out, double* h_entry) -> int {
-    finish_dot_kernel<<<1, 256, 0, ctx->stream>>>(g.grid, g.part, out, ctx->world > 1 ? nullptr : h_entry);
+    finish_dot_kernel<<<1, 256, 0, ctx->stream>>>(g.grid, g.part, out, ctx->collective ? nullptr : h_entry);
     CU(cudaGetLastError());
     ctx->launches++;
-    if (ctx->world > 1) {
+    if (ctx->collective) {
       TRY(comm_allreduce(ctx, out, 1, st));
       if (h_entry) {
         add_to_kernel<<<1, 1, 0, ctx->stream>>>(out, h_entry);
@@ -635,7 +635,7 @@ extern "C" int bo_sstep_gmres(bo_op op, const double* b, const double* x0, const
   uint64_t extra[4] = {0, 0, 0, 0};
   // ||A||_F (gmres.cpp:286-288)
   double a_fro2 = op->a_fro_local2;
-  if (ctx->world > 1) {
+  if (ctx->collective) {
     CU(cudaMemcpyAsync(g.gsum, &a_fro2, 8, cudaMemcpyHostToDevice, ctx->stream));
     TRY(comm_allreduce(ctx, g.gsum, 1, st));
     ctx->allreduces--;  // setup, not a ledger event

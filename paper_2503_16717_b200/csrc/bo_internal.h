@@ -20,6 +20,9 @@ struct bo_ctx_s {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_x = nullptr, ev_halo = nullptr;
   void* nccl = nullptr;  // ncclComm_t
+  // reductions go through the communicator (world > 1, or a size-1 NCCL
+  // communicator created on request: the NCCL path on a single GPU)
+  bool collective = false;
   bool has_comm = false;  // collectives through host callbacks (bo_ctx_create_comm)
   bo_comm_ops comm{};
   uint64_t n_global = 0, row_begin = 0, row_end = 0, n_local = 0, ld = 0;
@@ -220,10 +223,16 @@ constexpr int kSnapSlots = 64, kSnapStatus = OFF_STATUS, kSnapRin = OFF_RIN, kSn
               kSnapCoef = OFF_COEF, kSnapLen = OFF_COEF + LDC * 16;
 
 // NCCL, loaded lazily with dlopen (prefers the copy torch already mapped)
+struct NcclUniqueId {  // ncclUniqueId (nccl.h:39)
+  char internal[128];
+};
 struct NcclApi {
   void* h = nullptr;
   int (*GetUniqueId)(void* id) = nullptr;
-  int (*CommInitRank)(void** comm, int nranks, char id[128], int rank) = nullptr;
+  // ncclCommInitRank takes the 128-byte ncclUniqueId BY VALUE (nccl.h:171);
+  // declaring it as a pointer would pass the address where NCCL reads the
+  // struct from the stack
+  int (*CommInitRank)(void** comm, int nranks, NcclUniqueId id, int rank) = nullptr;
   int (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
   int (*CommDestroy)(void*) = nullptr;
   const char* (*GetErrorString)(int) = nullptr;

@@ -716,7 +716,7 @@ int sketch_to_host(bo_sketch th, const double* v, uint64_t ldv, int K, std::vect
                                                                          th->cnt);
     CU(cudaGetLastError());
     ctx->launches++;
-    if (ctx->world > 1) TRY(comm_allreduce(ctx, th->cnt, mc * K, st));
+    if (ctx->collective) TRY(comm_allreduce(ctx, th->cnt, mc * K, st));
     const double* res = th->cnt;
     if (th->kind != BO_SKETCH_COUNT) {
       const uint32_t ng = (uint32_t)(mh * K);

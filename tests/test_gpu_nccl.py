@@ -111,3 +111,43 @@ def test_nccl_sharded_sequence_and_gmres(gpu, orc):
         restarts, its, led, relres = res[r]["gmres"]
         assert (restarts, its, led) == (want.restarts, want.iterations, want.reduce)
         assert all(abs(g - w) <= env[i] * w for i, (g, w) in enumerate(zip(relres, want.relres)))
+
+
+def test_nccl_size1_communicator(gpu, orc):
+    """The library's NCCL path on ONE GPU: a context given an NCCL id with
+    world = 1 creates a size-1 communicator (ncclCommInitRank, which takes the
+    128-byte ncclUniqueId by value) and routes every ledger reduction through
+    ncclAllReduce followed by the 1-CTA finalize kernel (the multi-rank code
+    path), the GMRES norms through the same all-reduce, and a Count sketch's
+    bucket sums through it too.  A sum over one rank is the identity, so the
+    results must equal the fused single-GPU path bit for bit."""
+    n, k = 60000, 11
+    v = orc.gen_glued(n, 6, k, 1e6, 1e6, 7)
+    out = {}
+    for mode in ("plain", "nccl"):
+        ctx = gpu.Context(n, nccl_id=gpu.Context.nccl_unique_id() if mode == "nccl" else None)
+        res = {}
+        for intra, kind in ((0, None), (1, "gaussian"), (1, "count")):
+            th = gpu.SketchOperator.build(ctx, kind, n, k - 1, 1) if kind else None
+            st = gpu.BasisStore(ctx, 6 * k)
+            a0 = ctx.allreduces
+            for p in range(6):
+                gpu.bcgs2(st, ctx.from_host(v[:, p * k:(p + 1) * k]), intra, th, defer=True)
+            st.sync()
+            res[(intra, kind)] = (st.basis_copy(), st.r_copy(), st.ledger().counts, ctx.allreduces - a0)
+        ctx.close()
+        ctx = gpu.Context(100 * 100, nccl_id=gpu.Context.nccl_unique_id() if mode == "nccl" else None)
+        op = gpu.Operator.laplace(ctx, 2, 100)
+        _, rep = gpu.sstep_gmres_solve(op, ctx.from_host(np.ones(10000)), ctx.from_host(np.zeros(10000)), m=60, s=5,
+                                       shat=60, scheme="bcgs2_randcholqr", diagnostics=False)
+        res["gmres"] = (rep["restarts"], rep["iterations"], rep["reduce"], rep["restart_relres"])
+        op.close()
+        ctx.close()
+        out[mode] = res
+    for key in [(0, None), (1, "gaussian"), (1, "count")]:
+        q0, r0, led0, ar0 = out["plain"][key]
+        q1, r1, led1, ar1 = out["nccl"][key]
+        assert led0 == led1
+        assert ar0 == 0 and ar1 == sum(led1), (key, ar1, led1)  # one all-reduce per ledger event
+        assert np.array_equal(q0, q1) and np.array_equal(r0, r1), key
+    assert out["plain"]["gmres"] == out["nccl"]["gmres"]
