@@ -1,7 +1,7 @@
 """Device timeline of the C2 sequence (CUPTI activity records through
 torch.profiler): every kernel and memcpy of a few deferred steps with its
 start/end, so the gaps between launches (host enqueue, small copies, launch
-latency) can be read off.  python scripts/timeline.py [--steps 3] [--graph]"""
+latency) can be read off.  python scripts/timeline.py [--n N] [--steps 3] [--nccl1] [--verbose]"""
 import argparse
 import sys
 from pathlib import Path
@@ -19,9 +19,12 @@ ap.add_argument("--n", type=int, default=8_000_000)
 ap.add_argument("--s", type=int, default=10)
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--verbose", action="store_true")
+ap.add_argument("--nccl1", action="store_true",
+                help="size-1 NCCL communicator: every reduction through ncclAllReduce + the unfused finalize "
+                     "(the multi-rank code path on one GPU)")
 a = ap.parse_args()
 k = a.s + 1
-ctx = P.Context(a.n, device=0)
+ctx = P.Context(a.n, device=0, nccl_id=P.Context.nccl_unique_id() if a.nccl1 else None)
 torch.cuda.set_stream(ctx.stream)
 panels = bench.make_panels(P, ctx, argparse.Namespace(s=a.s, panels=6, kappa=1e2))
 theta = P.SketchOperator.build(ctx, "gaussian", a.n, a.s, 1)
