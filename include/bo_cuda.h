@@ -186,6 +186,9 @@ int bo_apply_inv_upper(bo_ctx ctx, const double* v, uint64_t ldv, uint64_t k, co
 /* --------------------------------------------------------- block-orth -- */
 /* BasisStore(n, capacity) (block_orth.hpp:27-102): device Q slab + host R/C */
 int bo_basis_create(bo_ctx ctx, uint64_t capacity, bo_basis* out, bo_status* st);
+/* The context keeps the largest destroyed slab (and one pinned snapshot area)
+ * for the next store it creates, as a GMRES solve creates an (m+1)-column
+ * store per call; they are freed with the context. */
 int bo_basis_destroy(bo_basis b);
 int bo_basis_reset(bo_basis b); /* back to an empty store, ledger zeroed */
 uint64_t bo_basis_cols(bo_basis b);

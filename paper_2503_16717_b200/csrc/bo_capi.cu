@@ -602,6 +602,15 @@ static int ctx_create_impl(int device, int rank, int world, const void* nccl_id,
     CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     c->own_stream = true;
   }
+  {
+    cudaMemPoolProps pp{};
+    pp.allocType = cudaMemAllocationTypePinned;
+    pp.location.type = cudaMemLocationTypeDevice;
+    pp.location.id = device;
+    CU(cudaMemPoolCreate(&c->pool, &pp));
+    uint64_t keep = ~0ULL;
+    CU(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  }
   CU(cudaMalloc(&c->counter, bo::kMaxRedCounters * sizeof(unsigned)));
   CU(cudaMemset(c->counter, 0, bo::kMaxRedCounters * sizeof(unsigned)));
 
@@ -655,11 +664,14 @@ extern "C" int bo_ctx_destroy(bo_ctx c) {
   cudaFreeHost(c->tiny_host);
   for (int i = 0; i < 3; ++i) cudaFree(c->scratch[i]);
   cudaFree(c->spare_buf);
+  cudaFree(c->spare_q);
+  if (c->spare_snap) cudaFreeHost(c->spare_snap);
   cudaFree(c->gen_plan.dev);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->ev_x) cudaEventDestroy(c->ev_x);
   if (c->ev_halo) cudaEventDestroy(c->ev_halo);
+  if (c->pool) cudaMemPoolDestroy(c->pool);
   delete c;
   return BO_OK;
 }
@@ -801,6 +813,10 @@ int gen_stream(bo_ctx ctx, uint64_t mt_seed, const std::vector<std::pair<uint64_
     const size_t nc = chunks.size();
     const int pw = bo::mt64::poly_words();
     std::vector<uint64_t> poly(pw), tab(2 * nc + nc + 1);
+    // cache x^target first: every later chunk of a segment then costs one
+    // multiplication mod phi (chained from its predecessor) instead of a full
+    // square-and-multiply (~300 ms -> a few ms for a 148-chunk plan)
+    bo::mt64::jump_poly(target, poly.data());
     std::vector<uint16_t> idx;
     idx.reserve(nc * 10240);
     for (size_t c = 0; c < nc; ++c) {
@@ -1314,12 +1330,24 @@ extern "C" int bo_basis_create(bo_ctx ctx, uint64_t capacity, bo_basis* out, bo_
   bo_basis b = new bo_basis_s();
   b->ctx = ctx;
   b->cap = capacity;
-  cudaError_t e = cudaMalloc(&b->q, std::max<uint64_t>(ctx->ld * capacity, 1) * 8);
-  if (e != cudaSuccess) {
-    delete b;
-    return set_st(st, BO_CUDA, 0, 0.0, "cudaMalloc(basis) failed: %s", cudaGetErrorString(e));
+  const size_t qbytes = std::max<uint64_t>(ctx->ld * capacity, 1) * 8;
+  if (ctx->spare_q && ctx->spare_q_bytes >= qbytes) {  // recycled from a destroyed store
+    b->q = ctx->spare_q;
+    b->q_bytes = ctx->spare_q_bytes;
+    ctx->spare_q = nullptr;
+  } else {
+    cudaError_t e = cudaMalloc(&b->q, qbytes);
+    if (e != cudaSuccess) {
+      delete b;
+      return set_st(st, BO_CUDA, 0, 0.0, "cudaMalloc(basis) failed: %s", cudaGetErrorString(e));
+    }
+    b->q_bytes = qbytes;
   }
   cudaMemsetAsync(b->q, 0, ctx->ld * capacity * 8, ctx->stream);
+  if (ctx->spare_snap) {
+    b->snap = ctx->spare_snap;
+    ctx->spare_snap = nullptr;
+  }
   b->r.assign(capacity * capacity, 0.0);
   b->c.assign(capacity * capacity, 0.0);
   b->seeded.assign(capacity, 0);
@@ -1329,9 +1357,19 @@ extern "C" int bo_basis_create(bo_ctx ctx, uint64_t capacity, bo_basis* out, bo_
 extern "C" int bo_basis_destroy(bo_basis b) {
   if (!b) return BO_OK;
   basis_drain(b);
-  if (b->snap) cudaFreeHost(b->snap);
-  cudaStreamSynchronize(b->ctx->stream);
-  cudaFree(b->q);
+  bo_ctx ctx = b->ctx;
+  cudaStreamSynchronize(ctx->stream);
+  if (b->snap) {
+    if (!ctx->spare_snap) ctx->spare_snap = b->snap;  // keep one pinned snapshot area
+    else cudaFreeHost(b->snap);
+  }
+  if (!ctx->spare_q || ctx->spare_q_bytes < b->q_bytes) {  // keep the larger slab for the next store
+    if (ctx->spare_q) cudaFree(ctx->spare_q);
+    ctx->spare_q = b->q;
+    ctx->spare_q_bytes = b->q_bytes;
+  } else {
+    cudaFree(b->q);
+  }
   delete b;
   return BO_OK;
 }

@@ -443,11 +443,11 @@ int recover_panel(Gm& g, bo_basis b, const double* v, uint64_t ldv, int w, bool 
   const bool eff = overlap && b->cols > 0;
   const uint64_t hi = b->cols - (eff ? 1 : 0);
   double* vhat = nullptr;
-  CU(cudaMallocAsync((void**)&vhat, ctx->ld * w * 8, ctx->stream));
+  CU(ctx_alloc(ctx, (void**)&vhat, ctx->ld * w * 8));
   std::vector<double> pc(std::max<uint64_t>(hi, 1) * w, 0.0);
   int rc = bo_bcgs_project_range(b, v, ldv, w, 0, hi, vhat, ctx->ld, pc.data(), st);
   if (rc) {
-    cudaFreeAsync(vhat, ctx->stream);
+    ctx_free(ctx, vhat);
     return rc;
   }
   // recursive CholQR writes the kept columns straight into the slab at `hi`
@@ -459,7 +459,7 @@ int recover_panel(Gm& g, bo_basis b, const double* v, uint64_t ldv, int w, bool 
   bo_status rst;
   rc = bo_recursive_cholqr(ctx, vhat, ctx->ld, w, qdst, ctx->ld, coeffs.data(), kept.data(), &nk, disc.data(),
                            dn.data(), &nd, &depth, b->ledger, &rst);
-  cudaFreeAsync(vhat, ctx->stream);
+  ctx_free(ctx, vhat);
   if (rc == BO_CUDA || rc == BO_NCCL) {
     if (st) *st = rst;
     return rc;
@@ -556,7 +556,7 @@ int diagnostics(Gm& g, bo_basis b, const hd::Mat& H, size_t q_in, double a_fro, 
   }
   // Arnoldi residual: column j: A q_j - Q h_j
   double* hd = nullptr;
-  CU(cudaMallocAsync((void**)&hd, std::max<size_t>(H.r, 1) * 8, ctx->stream));
+  CU(ctx_alloc(ctx, (void**)&hd, std::max<size_t>(H.r, 1) * 8));
   double total = 0.0;
   for (size_t j = 0; j < q_in; ++j) {
     TRY(op_apply(g.op, b->q + j * ctx->ld, aq, st));
@@ -571,7 +571,7 @@ int diagnostics(Gm& g, bo_basis b, const hd::Mat& H, size_t q_in, double a_fro, 
     TRY(reduce_sum(g, g.grid, &s, st));
     total += s;
   }
-  cudaFreeAsync(hd, ctx->stream);
+  ctx_free(ctx, hd);
   *arn = std::sqrt(total) / a_fro;
   return BO_OK;
 }
@@ -609,27 +609,32 @@ extern "C" int bo_sstep_gmres(bo_op op, const double* b, const double* x0, const
   g.op = op;
   g.grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(ctx->num_sms * 2, (nl + 255) / 256));
   double *r = nullptr, *ax = nullptr, *panel = nullptr, *q1 = nullptr;
-  CU(cudaMalloc(&g.part, 4096 * 8));
-  CU(cudaMalloc(&g.gsum, 64));
-  CU(cudaMalloc(&g.ydev, (cfg->m + 2) * 8));
-  CU(cudaMalloc(&r, ld * 8));
-  CU(cudaMalloc(&ax, ld * 8));
-  CU(cudaMalloc(&q1, ld * 8));
-  CU(cudaMalloc(&panel, ld * K * 8));
-  CU(cudaMemsetAsync(panel, 0, ld * K * 8, ctx->stream));
-  CU(cudaMemcpyAsync(x, x0, nl * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+  // per-solve scratch from the ctx pool (stream-ordered, kept reserved between solves)
   struct Free {
+    bo_ctx c;
     std::vector<void*> p;
     ~Free() {
-      for (void* q : p) cudaFree(q);
+      for (void* q : p) ctx_free(c, q);
     }
-  } fr{{g.part, g.gsum, g.ydev, r, ax, q1, panel}};
+  } fr{ctx, {}};
+  auto scratch = [&](void** p, size_t bytes) {
+    const cudaError_t e = ctx_alloc(ctx, p, bytes);
+    if (e == cudaSuccess) fr.p.push_back(*p);
+    return e;
+  };
+  CU(scratch((void**)&g.part, 4096 * 8));
+  CU(scratch((void**)&g.gsum, 64));
+  CU(scratch((void**)&g.ydev, (cfg->m + 2) * 8));
+  CU(scratch((void**)&r, ld * 8));
+  CU(scratch((void**)&ax, ld * 8));
+  CU(scratch((void**)&q1, ld * 8));
+  CU(scratch((void**)&panel, ld * K * 8));
+  CU(cudaMemsetAsync(panel, 0, ld * K * 8, ctx->stream));
+  CU(cudaMemcpyAsync(x, x0, nl * 8, cudaMemcpyDeviceToDevice, ctx->stream));
   double *wbuf = nullptr, *cgsdev = nullptr;  // standard GMRES: w and the Hessenberg / dot scratch
   if (cgs2) {
-    CU(cudaMalloc(&wbuf, ld * 8));
-    CU(cudaMalloc(&cgsdev, ((cfg->m + 1) * cfg->m + cfg->m + 2) * 8));
-    fr.p.push_back(wbuf);
-    fr.p.push_back(cgsdev);
+    CU(scratch((void**)&wbuf, ld * 8));
+    CU(scratch((void**)&cgsdev, ((cfg->m + 1) * cfg->m + cfg->m + 2) * 8));
   }
 
   uint64_t extra[4] = {0, 0, 0, 0};

@@ -65,8 +65,27 @@ struct bo_ctx_s {
   // one recycled tall sketch buffer (a Gaussian sketch is rebuilt every
   // restart cycle: cudaMalloc/cudaFree of ~1.4 GB each time would stall)
   void* spare_buf = nullptr;
+  // one recycled basis slab and pinned snapshot area: a GMRES solve creates a
+  // store of m + 1 columns (3.9 GB at 8e6 rows), and cudaMalloc / cudaFree /
+  // cudaMallocHost of that every solve cost milliseconds
+  double* spare_q = nullptr;
+  size_t spare_q_bytes = 0;
+  double* spare_snap = nullptr;
   size_t spare_bytes = 0;
+  // stream-ordered pool for per-solve scratch (residual / panel vectors of a
+  // GMRES solve, MPK and sketch temporaries): released memory stays reserved
+  // (release threshold = max), so repeated solves allocate without a device
+  // synchronisation or a page-mapping stall
+  cudaMemPool_t pool = nullptr;
 };
+
+// scratch from the ctx pool, ordered on the ctx stream
+inline cudaError_t ctx_alloc(bo_ctx_s* c, void** p, size_t bytes) {
+  return cudaMallocFromPoolAsync(p, bytes, c->pool, c->stream);
+}
+inline void ctx_free(bo_ctx_s* c, void* p) {
+  if (p) cudaFreeAsync(p, c->stream);
+}
 
 struct bo_sketch_s {
   bo_ctx ctx = nullptr;
@@ -91,6 +110,7 @@ struct bo_basis_s {
   bo_ctx ctx = nullptr;
   uint64_t cap = 0, cols = 0;
   double* q = nullptr;  // device slab ld x cap
+  size_t q_bytes = 0;   // its allocation (a recycled slab may be larger)
   std::vector<double> r, c;  // host cap x cap
   std::vector<char> seeded;
   std::vector<uint64_t> bounds;

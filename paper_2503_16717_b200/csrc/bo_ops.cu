@@ -666,11 +666,11 @@ static int count_sort(bo_sketch th, bo_status* st) {
   CU(cudaMalloc(&th->perm, std::max<size_t>(n, 1) * 4));
   CU(cudaMalloc(&th->boff, ((size_t)mc + 1) * 4));
   CU(cudaMalloc(&th->cnt, ((size_t)mc * 16 + (size_t)th->mhat * 16) * 8));
-  CU(cudaMalloc(&keys, std::max<size_t>(n, 1) * 4 * 3 + ((size_t)mc + 1) * 4));
+  CU(ctx_alloc(ctx, (void**)&keys, std::max<size_t>(n, 1) * 4 * 3 + ((size_t)mc + 1) * 4));
   vals = keys + std::max<uint32_t>(n, 1);
   keys2 = vals + std::max<uint32_t>(n, 1);
   hist = keys2 + std::max<uint32_t>(n, 1);
-  CU(cudaMalloc(&tmp, std::max(tb_sort, tb_scan)));
+  CU(ctx_alloc(ctx, &tmp, std::max(tb_sort, tb_scan)));
   CU(cudaMemsetAsync(hist, 0, ((size_t)mc + 1) * 4, ctx->stream));
   if (n) {
     count_keys_kernel<<<std::max(1, std::min(ctx->num_sms * 8, (int)((n + 255) / 256))), 256, 0, ctx->stream>>>(
@@ -679,9 +679,9 @@ static int count_sort(bo_sketch th, bo_status* st) {
     CU(cub::DeviceRadixSort::SortPairs(tmp, tb_sort, keys, keys2, vals, th->perm, (int)n, 0, bits, ctx->stream));
   }
   CU(cub::DeviceScan::ExclusiveSum(tmp, tb_scan, hist, th->boff, (int)mc + 1, ctx->stream));
+  ctx_free(ctx, tmp);
+  ctx_free(ctx, keys);
   CU(cudaStreamSynchronize(ctx->stream));
-  cudaFree(tmp);
-  cudaFree(keys);
   return BO_OK;
 }
 
@@ -1175,7 +1175,7 @@ int rec_impl(bo_ctx ctx, const double* v, uint64_t ldv, int w, const std::vector
   // rest = v[:, good:] - q_good R12
   double* rest = nullptr;
   const size_t ldr = ctx->ld;
-  CU(cudaMallocAsync((void**)&rest, ldr * (w - good) * 8, ctx->stream));
+  CU(ctx_alloc(ctx, (void**)&rest, ldr * (w - good) * 8));
   CU(cudaMemcpyAsync(T_(ctx, OFF_C1), r12.data(), r12.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
   PassReq u{};
   u.kind = PK_UPD_ST;
@@ -1193,7 +1193,7 @@ int rec_impl(bo_ctx ctx, const double* v, uint64_t ldv, int w, const std::vector
   acc.depth++;
   std::vector<uint64_t> rest_ids(ids.begin() + good, ids.end());
   const int rc = rec_impl(ctx, rest, ldr, w - good, rest_ids, acc, ledger, st);
-  cudaFreeAsync(rest, ctx->stream);
+  ctx_free(ctx, rest);
   return rc;
 }
 }  // namespace

@@ -9,7 +9,8 @@
 // p(x) = x^J mod phi(x),
 //     g[J + t] = XOR_{k : p_k = 1} g[k + t]      for every t >= 0,
 // so the 312-word window starting at J is an XOR of windows of the first
-// 20248 generated words.  phi is recovered once with Berlekamp-Massey; the
+// 20248 generated words.  phi was recovered with Berlekamp-Massey and is
+// compiled in (mt64_phi_table.h, scripts/gen_mt64_phi.sh); the
 // seed-independent polynomials x^J mod phi are computed with carry-less
 // multiplication + Barrett reduction and cached for the process lifetime.
 //
@@ -23,6 +24,9 @@
 #include <vector>
 
 #include "mt64_jump.h"
+#ifndef BO_MT64_NO_PHI_TABLE
+#include "mt64_phi_table.h"
+#endif
 
 #if defined(__x86_64__)
 #include <immintrin.h>
@@ -202,18 +206,36 @@ static Poly mulmod(const Field& f, const Poly& a, const Poly& b) {
   return reduce(f, t);
 }
 
-static void init_field(Field& f) {
-  // 2*deg + margin bits of the LSB of the untempered stream (any nonzero seed)
+// phi(x) recovered from the generator itself: Berlekamp-Massey over the LSB of
+// 2 deg + 64 untempered words (any nonzero seed).  Empty if the recovered
+// degree is not 19937.
+static Poly phi_by_berlekamp_massey() {
   Mt mt(5489ULL);
   const long N = 2 * kDeg + 64;
   std::vector<uint8_t> bits(N);
   for (long i = 0; i < N; ++i) bits[i] = (uint8_t)(mt.raw() & 1);
   int L = 0;
   const Poly C = berlekamp_massey(bits, L);
+  if (L != kDeg) return Poly();
   // phi(x) = x^L C(1/x): coefficient of x^(L-j) is C[j]
-  f.phi.assign(kWords + 1, 0);
+  Poly phi(kWords + 1, 0);
   for (int j = 0; j <= L; ++j)
-    if (get_bit(C, j)) flip_bit(f.phi, L - j);
+    if (get_bit(C, j)) flip_bit(phi, L - j);
+  return phi;
+}
+
+static void init_field(Field& f) {
+#ifdef BO_MT64_NO_PHI_TABLE
+  f.phi = phi_by_berlekamp_massey();
+#else
+  // the table scripts/gen_mt64_phi.sh printed from phi_by_berlekamp_massey()
+  // (0.5-0.7 s saved per process); the jump-window tests check the result
+  // against the sequential generator
+  f.phi.assign(kMt64Phi, kMt64Phi + sizeof(kMt64Phi) / sizeof(kMt64Phi[0]));
+#endif
+  f.ready = f.phi.size() == (size_t)kWords + 1 && get_bit(f.phi, kDeg) && get_bit(f.phi, 0) &&
+            f.phi[kWords] == 0 && (f.phi[kDeg >> 6] >> ((kDeg & 63) + 1)) == 0;
+  if (!f.ready) return;
   // mu = floor(x^(2d) / phi) by long division
   const long top = 2L * kDeg;
   Poly rem((top + 64) / 64 + 1, 0);
@@ -232,7 +254,6 @@ static void init_field(Field& f) {
       if (bs && w + ws + 1 < (long)rem.size()) rem[w + ws + 1] ^= v >> (64 - bs);
     }
   }
-  f.ready = (L == kDeg);
 }
 
 // x^J mod phi by square-and-multiply (multiply by x is a shift + reduce)
