@@ -241,47 +241,87 @@ int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st) {
   // (a third stage for the other passes measured no better: QTX / UPD_SKG_ST
   // within +-2% at every p, sequence +0.3 ms at 3 stages)
   const int want_hi = (ki.npre > 0 && !rowg_kind) ? ns_pre : 2;
-  for (int want_ns : {want_hi, 2, 1}) {
-    for (int tt : {256, 128, 64}) {
-      if (T) break;
-      if (want_ns > 2 && tt < 128 && !tile_env) continue;
-      if (r.exact && tt != 64) continue;
-      if (tile_env && tt != tile_env) continue;
-      if (tt > tile_max) continue;
-      if (rowg_kind && tt != 128 && !tile_env) continue;
-      const int S = tile_stride(tt), nsub = tt / tile_sub_rows(tt);
-      // row-mode Gram (bo_pass.cuh ROWG): unpadded stages, no X tile
-      const bool rowg = rowg_kind && tt == 128;
-      const StageLayout SL = stage_layout(r.K, (ki.qtx || ki.upd) ? r.p : 0, ki.sk == SK_GAUSS ? mh : 0,
-                                          ki.sk == SK_COUNT, tt, !rowg);
-      const size_t stage = (size_t)SL.stage * 8;
-      // X tile.  The kernel only uses one for a post-solve without an update
-      // (bo_pass.cuh XT && !XIN): update and pre-solve passes compute X in
-      // place in the stage.  The reservation is kept for pre-solve passes as a
-      // cap on their ring: releasing it lets them pick 256-row tiles and deeper
-      // rings, which measured slower (P1_ST 227 -> 252 us, C2 sequence +0.4 ms).
-      const bool xt = (ki.npre > 0 || ki.npost > 0) && !rowg && !(ki.upd && ki.npre == 0);
-      // row-major copies of the solve factors (bo_pass.cuh RFT) in K-specialised solve passes
-      const bool rft = !r.exact && (ki.npre > 0 || ki.npost > 0) && (r.K == 6 || r.K == 11 || r.K == 13 || r.K == 16);
-      const size_t fixed = (xt ? 2 * (size_t)nt * 8 * S * 8 * nsub : 0) + (3 * 256 + 48 + (rft ? 3 * 256 : 0)) * 8 +
-                           (ki.sk == SK_COUNT ? (size_t)mh * r.K * 8 : 0) + 3 * kMaxStages * 8;
-      const size_t need_red = (size_t)consumer_warps(ki.upd, pre_qtx, pre_upd) * dm_len * 8;
-      const size_t need_fin = (1536 + (size_t)std::max(mh, 32) * 16 + 64) * 8;  // finalize_dev scratch
-      if (avail <= fixed) continue;
-      int ns = (int)std::min<size_t>(kMaxStages, (avail - fixed) / stage);
-      if (rowg) ns = ns / consumer_warps(false) * consumer_warps(false);  // one private sub-ring per warp
-      if (ns < want_ns) continue;
-      const size_t r0 = round_up(std::max({(size_t)ns * stage, need_red, need_fin}), 128);
-      if (r0 + fixed > avail) continue;
-      T = tt;
-      NS = ns;
-      region0 = r0;
-      total = r0 + fixed;
+  // Decoupled rings (bo_pass.cuh DEC): pre-solve passes with a projection
+  // range keep their panel tiles in a separate ring, vla tiles deeper than
+  // the basis ring.  BO_DEC_RING=0 at build time restores joint stages.
+  const bool dec_ok = BO_DEC_RING && BO_PRODUCER_WARP && ki.npre > 0 && (ki.qtx || ki.upd) && !r.exact;
+  static const int vla = [] {
+    const char* e = getenv("BO_VLA");
+    return e ? std::max(1, atoi(e)) : 1;  // measured: 1 beats 2, 3 and 4
+  }();
+  static const int dec_env = [] {
+    const char* e = getenv("BO_DEC");  // -1: never, 1: whenever eligible, 0 (default): when joint stages give <= 2
+    return e ? atoi(e) : 0;
+  }();
+  int NSV = 0;
+  auto choose = [&](bool dec) {
+    T = 0;
+    NS = NSV = 0;
+    for (int want_ns : {want_hi, 2, 1}) {
+      for (int tt : {256, 128, 64}) {
+        if (T) break;
+        if (want_ns > 2 && tt < 128 && !tile_env) continue;
+        if (r.exact && tt != 64) continue;
+        if (tile_env && tt != tile_env) continue;
+        if (tt > tile_max) continue;
+        if (rowg_kind && tt != 128 && !tile_env) continue;
+        const int S = tile_stride(tt), nsub = tt / tile_sub_rows(tt);
+        // row-mode Gram (bo_pass.cuh ROWG): unpadded stages, no X tile
+        const bool rowg = rowg_kind && tt == 128;
+        const StageLayout SL = stage_layout(r.K, (ki.qtx || ki.upd) ? r.p : 0, ki.sk == SK_GAUSS ? mh : 0,
+                                            ki.sk == SK_COUNT, tt, !rowg);
+        const size_t stage = (size_t)SL.stage * 8;
+        // X tile.  The kernel only uses one for a post-solve without an update
+        // (bo_pass.cuh XT && !XIN): update and pre-solve passes compute X in
+        // place in the stage.  The reservation is kept for pre-solve passes as a
+        // cap on their ring: releasing it lets them pick 256-row tiles and deeper
+        // rings, which measured slower (P1_ST 227 -> 252 us, C2 sequence +0.4 ms).
+        const bool xt = (ki.npre > 0 || ki.npost > 0) && !rowg && !(ki.upd && ki.npre == 0) && !dec;
+        // row-major copies of the solve factors (bo_pass.cuh RFT) in K-specialised solve passes
+        const bool rft = !r.exact && (ki.npre > 0 || ki.npost > 0) && (r.K == 6 || r.K == 11 || r.K == 13 || r.K == 16);
+        const size_t fixed = (xt ? 2 * (size_t)nt * 8 * S * 8 * nsub : 0) + (3 * 256 + 48 + (rft ? 3 * 256 : 0)) * 8 +
+                             (ki.sk == SK_COUNT ? (size_t)mh * r.K * 8 : 0) + 4 * kMaxStages * 8;
+        const size_t need_red = (size_t)consumer_warps(ki.upd, pre_qtx, pre_upd) * dm_len * 8;
+        const size_t need_fin = (1536 + (size_t)std::max(mh, 32) * 16 + 64) * 8;  // finalize_dev scratch
+        if (avail <= fixed) continue;
+        int ns = (int)std::min<size_t>(kMaxStages, (avail - fixed) / stage);
+        size_t ring = (size_t)ns * stage;
+        int nsv = 0;
+        if (dec) {
+          // basis ring of ns slots, panel ring of ns + vla slots
+          const size_t vb = (size_t)SL.offQ * 8, qb = stage - vb;
+          ns = avail - fixed > vla * vb ? (int)std::min<size_t>(kMaxStages - vla, (avail - fixed - vla * vb) / (qb + vb))
+                                        : 0;
+          nsv = ns + vla;
+          ring = (size_t)ns * qb + (size_t)nsv * vb;
+        }
+        if (rowg) ns = ns / consumer_warps(false) * consumer_warps(false);  // one private sub-ring per warp
+        if (ns < want_ns) continue;
+        const size_t r0 = round_up(std::max({ring, need_red, need_fin}), 128);
+        if (r0 + fixed > avail) continue;
+        T = tt;
+        NS = ns;
+        NSV = nsv;
+        region0 = r0;
+        total = r0 + fixed;
+      }
     }
+  };
+  // Decoupled rings (bo_pass.cuh DEC) where joint stages leave only a double
+  // buffer: measured on the C2 sequence (scripts/ab_tail.sh), P2_QTX at
+  // p = 44 / 55 734 / 810 -> 652 / 737 us and P2_UPD_GRAM_ST 883 / 939 -> 847 /
+  // 908 us, while at p <= 33 (3-5 joint stages) they were 3-5% slower.
+  choose(dec_ok && dec_env > 0);
+  if (dec_ok && dec_env == 0 && T && NS <= 2) {
+    const int T0 = T, NS0 = NS;
+    const size_t r00 = region0, tot0 = total;
+    choose(true);
+    if (!T) T = T0, NS = NS0, NSV = 0, region0 = r00, total = tot0;
   }
   if (T == 0) return set_st(st, BO_INVALID, 0, 0.0, "pass does not fit in shared memory");
   if (total > avail) return set_st(st, BO_INVALID, 0, 0.0, "pass does not fit in shared memory (%zu bytes)", total);
   a.nstages = NS;
+  a.nstages_v = NSV;
   {
     // bytes to keep in flight per SM (L2 prefetch + ring): loaded HBM latency
     // x per-SM bandwidth with margin (~5 us x 44 GB/s)

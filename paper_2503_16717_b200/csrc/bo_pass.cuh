@@ -48,6 +48,32 @@
 #ifndef BO_STORE_SPREAD
 #define BO_STORE_SPREAD 1
 #endif
+// Tail columns on FP64 FMAs (see TN in pass_kernel), per site: the projection
+// contraction Q^T X when it has at least BO_TAIL_QTX_MIN 8-column Q tiles, the
+// update X - QC with at least BO_TAIL_UPD_MIN, the Gram X^T X.  0: DMMA.
+#ifndef BO_DFMA_TAIL
+#define BO_DFMA_TAIL 1
+#endif
+#ifndef BO_TAIL_QTX
+#define BO_TAIL_QTX 1
+#endif
+#ifndef BO_TAIL_QTX_MIN
+#define BO_TAIL_QTX_MIN 4
+#endif
+#ifndef BO_TAIL_UPD
+#define BO_TAIL_UPD 0
+#endif
+#ifndef BO_TAIL_UPD_MIN
+#define BO_TAIL_UPD_MIN 4
+#endif
+#ifndef BO_TAIL_GRAM
+#define BO_TAIL_GRAM 0
+#endif
+// Pre-solve passes with a projection range: separate panel (V) and basis (Q)
+// rings, the panel ring deeper (see DEC in pass_kernel); 0: one ring of joint stages
+#ifndef BO_DEC_RING
+#define BO_DEC_RING 1
+#endif
 #if BO_PHASE_PROF
 #define PP_T0() long long pp_t = clock64()
 #define PP_MARK(i)                      \
@@ -339,6 +365,22 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
   constexpr bool ROWG = GRAM && !QTX && !UPD && SK == SK_NONE && !STORE && NPOST == 0 && NPRE > 0 && KC > 0 &&
                         KC <= 11 && T == 128;
   constexpr int NG = ROWG ? KC * (KC + 1) / 2 : 1;
+  // Tail columns.  With 8 < K <= 11 (K = 11 at s = 10) the second 8-column
+  // DMMA tile would carry 16 - K zero columns: 5 of its 8 at K = 11.  Its
+  // TN = K - 8 live columns instead go through FP64 FMAs on the fragments
+  // already in registers.  In a contraction, lane (g, t4) holds A[g][t4] (row
+  // t4 of the k-step), so TN extra shared loads of X[row t4][8..K) feed TN FMAs
+  // per A fragment.  In the update, lane (g, t4) holds Q[row g][col t4] and the
+  // coefficients -C[t4][8..K) in registers; the TN partial sums are reduced
+  // over the 4 t4 lanes per row group.  Per k-step and 8 rows: 3 DFMA (about
+  // 7 FP64-pipe cycles per sub-partition) instead of one DMMA (16 cycles).
+  constexpr int TN = (BO_DFMA_TAIL && NT == 2 && KC > 8 && KC <= 11 && !EXACT && SK != SK_GAUSS) ? KC - 8 : 0;
+  constexpr int TNA = TN ? TN : 1;         // array extents
+  constexpr int NPAIR = TN * (TN + 1) / 2; // tail x tail Gram entries, one per lane group g
+  constexpr bool TQ = TN && QTX && BO_TAIL_QTX;   // per site (measured: the tail pays only where
+  constexpr bool TU = TN && UPD && BO_TAIL_UPD;   // the DMMA work per k-step is large enough)
+  constexpr bool TG = TN && GRAM && BO_TAIL_GRAM;
+  constexpr int NTG = TG ? 1 : NT;                // Gram column tiles on DMMA
   static_assert(!(QTX && UPD), "a pass either projects or updates");
   static_assert(!STORE || XT, "stores come from the X tile");
   static_assert(!SPLIT || T <= GAW * 128, "row-solve group handles at most four rows per thread");
@@ -355,8 +397,33 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
   // offset of row r of a P-column operand block (see TileGeom): c * S + so(r, P)
   auto so = [](int r, int P) { return NSUB > 1 ? (r >> 7) * P * S + (r & 127) : r; };
   const StageLayout L = stage_layout(K, ncolQ, ncolT, SK == SK_COUNT, T, !ROWG);
-  const int NS = a.nstages;
+  // Decoupled rings (pre-solve passes with a projection range).  With joint
+  // stages a stage is held from its arrival through the row solve AND the
+  // U/S/R work, so at p = 55 (76 KB stages, 2 fit) the basis block of the next
+  // tile is issued only after both: the solve latency is exposed once per tile
+  // and the HBM stream idles (ncu: solve warps 67% of their samples waiting
+  // for data, the producer half its time waiting for a free stage).  Here the
+  // panel tiles (K columns, 17 KB) live in their own ring, VLA = NSV - NS
+  // tiles ahead of the basis ring, so a tile's rows are solved before its
+  // basis block lands and a basis slot is held only for the U/S/R work, as in
+  // the passes without a solve.  Tile it uses basis slot it % NS and panel slot
+  // it % NSV; the producer issues basis tile it and panel tile it + VLA when
+  // the group releases tile it - NS, which frees both slots.
+  // The host picks it per launch (a.nstages_v > 0) where joint stages would
+  // leave only two in the ring (p >= 44 at K = 11); with deeper joint rings it
+  // measured slower.
+  constexpr bool DEC = BO_DEC_RING && SPLIT && !ROWG && (QTX || UPD) && BO_PRODUCER_WARP;
+  const bool dec = DEC && a.nstages_v > 0;
+  const int NS = a.nstages;                    // joint ring depth, or the basis ring's (dec)
+  const int NSV = dec ? a.nstages_v : NS;      // panel ring depth (dec)
+  const int VLA = NSV - NS;                    // panel lookahead in tiles (DEC)
+  const int vsz = L.offQ, qsz = L.stage - L.offQ;  // DEC slot sizes (doubles)
   double* stages = reinterpret_cast<double*>(smem_raw);
+  // V block of panel slot sv, and the basis-side blocks (Q, Theta, codes) of slot sq
+  auto slotV = [&](int sv) { return dec ? stages + (size_t)sv * vsz : stages + (size_t)sv * L.stage + L.offV; };
+  auto slotQ = [&](int sq) {
+    return dec ? stages + (size_t)NSV * vsz + (size_t)sq * qsz : stages + (size_t)sq * L.stage + L.offQ;
+  };
   double* xtile = stages + a.region0_dbl;                         // [2][NSUB][KP][S]
   double* rfac = xtile + ((XT && !ROWG && !XIN) ? 2 * NSUB * KP * S : 0); // [3][256]
   double* rinv = rfac + 3 * 256;                                  // [3][16]
@@ -367,26 +434,37 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
   uint64_t* full = bars;
   uint64_t* empty = bars + kMaxStages;
   uint64_t* solved = bars + 2 * kMaxStages;  // pre-solve passes: X of the stage is ready
+  uint64_t* fullv = bars + 3 * kMaxStages;   // DEC: panel slot loaded
   __shared__ int s_skip;
 
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
       ptx::mbar_init(&full[s], 1);
-      if (SPLIT) ptx::mbar_init(&solved[s], GAW);
-      if (BO_PRODUCER_WARP) ptx::mbar_init(&empty[s], ROWG ? 1 : NW);
+      // DEC: only the U/S/R group releases (the solve warps are done with a
+      // tile before the group starts it)
+      if (BO_PRODUCER_WARP) ptx::mbar_init(&empty[s], ROWG ? 1 : (dec ? GW : NW));
       else reinterpret_cast<unsigned*>(&empty[s])[0] = 0u;  // arrival counter
+    }
+    for (int s = 0; s < NSV; ++s) {
+      if (SPLIT) ptx::mbar_init(&solved[s], GAW);
+      if (dec) ptx::mbar_init(&fullv[s], 1);
     }
     ptx::fence_mbar_init();
   }
   if (SK == SK_COUNT)
     for (int e = tid; e < mh * K; e += blockDim.x) cacc[e] = 0.0;
   // zero padding columns (never written by TMA or the phases)
+  for (int s = 0; s < (ROWG ? 0 : NSV); ++s)
+    for (int q = 0; q < NSUB; ++q) {
+      double* sv = slotV(s);
+      for (int e = tid; e < (KP - K) * S; e += blockDim.x) sv[q * KP * S + K * S + e] = 0.0;
+    }
   for (int s = 0; s < (ROWG ? 0 : NS); ++s)
     for (int q = 0; q < NSUB; ++q) {
-      double* st = stages + (size_t)s * L.stage;
-      for (int e = tid; e < (KP - K) * S; e += blockDim.x) st[L.offV + q * KP * S + K * S + e] = 0.0;
-      for (int e = tid; e < (mq * 8 - ncolQ) * S; e += blockDim.x) st[L.offQ + q * mq * 8 * S + ncolQ * S + e] = 0.0;
-      for (int e = tid; e < (ms * 8 - ncolT) * S; e += blockDim.x) st[L.offT + q * ms * 8 * S + ncolT * S + e] = 0.0;
+      double* sq = slotQ(s);
+      for (int e = tid; e < (mq * 8 - ncolQ) * S; e += blockDim.x) sq[q * mq * 8 * S + ncolQ * S + e] = 0.0;
+      for (int e = tid; e < (ms * 8 - ncolT) * S; e += blockDim.x)
+        sq[(L.offT - L.offQ) + q * ms * 8 * S + ncolT * S + e] = 0.0;
     }
   if (XT && !ROWG && !XIN)
     for (int b = 0; b < 2 * NSUB; ++b)
@@ -408,6 +486,20 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
     for (int e = tid; e < 3 * 256; e += blockDim.x) {
       const int f = e / 256, j = (e % 256) / 16, l = e % 16;  // Rt_f[j*16 + l]
       rft[e] = l > j ? rfac[f * 256 + j + l * kRld] : (l == j ? rinv[f * 16 + j] : 0.0);
+    }
+  }
+  // Tail update coefficients (TN > 0): ctls[r * 4 + c] = -C[r][8 + c], r < 64, in
+  // the R-factor slot this pass does not use (a pre-solve pass has no post
+  // factor; a post-solve pass no pre factor).  A lane reads its row t4 of a
+  // k-step as one 16-byte and one 8-byte shared load (4 addresses per warp);
+  // 48 coefficient registers per thread would spill at the 168-register cap.
+  static_assert(!(TU && NPRE > 0 && NPOST > 0), "tail coefficients need a free R-factor slot");
+  double* ctls = rfac + (NPOST > 0 ? 0 : 512);
+  if (TU) {
+    __syncthreads();  // rinv / rft have read the slot
+    for (int e = tid; e < 256; e += blockDim.x) {
+      const int r = e >> 2, c = e & 3;
+      ctls[e] = (r < p && c < TN) ? -a.Cm[r + (8 + c) * a.ldc] : 0.0;
     }
   }
   __syncthreads();
@@ -448,6 +540,27 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
       if (ncolT) ptx::tma_load_2d(st + L.offT + q * ms * 8 * S, &tmT, (int)row0 + 128 * q, 0, &full[s]);
     }
     if (SK == SK_COUNT) ptx::bulk_g2s(st + L.offC, a.code + row0, cb, &full[s]);
+  };
+  // DEC: the panel tile into panel slot sv, the basis-side blocks into basis slot sq
+  auto issue_v = [&](int it, int sv) {
+    const long long row0 = (long long)(blockIdx.x + (long long)it * gridDim.x) * T;
+    double* dst = slotV(sv);
+    ptx::mbar_arrive_expect_tx(&fullv[sv], (uint32_t)(NSUB * S * 8 * K));
+#pragma unroll
+    for (int q = 0; q < NSUB; ++q) ptx::tma_load_2d(dst + q * KP * S, &tmV, (int)row0 + 128 * q, 0, &fullv[sv]);
+  };
+  auto issue_q = [&](int it, int sq) {
+    const long long row0 = (long long)(blockIdx.x + (long long)it * gridDim.x) * T;
+    const long long valid = nrows - row0 < T ? nrows - row0 : T;
+    const uint32_t cb = (SK == SK_COUNT) ? (uint32_t)(((valid + 3) & ~3LL) * 4) : 0u;
+    double* dst = slotQ(sq);
+    ptx::mbar_arrive_expect_tx(&full[sq], (uint32_t)(NSUB * S * 8 * (ncolQ + ncolT)) + cb);
+#pragma unroll
+    for (int q = 0; q < NSUB; ++q) {
+      if (ncolQ) ptx::tma_load_2d(dst + q * mq * 8 * S, &tmQ, (int)row0 + 128 * q, 0, &full[sq]);
+      if (ncolT) ptx::tma_load_2d(dst + (L.offT - L.offQ) + q * ms * 8 * S, &tmT, (int)row0 + 128 * q, 0, &full[sq]);
+    }
+    if (SK == SK_COUNT) ptx::bulk_g2s(dst + (L.offC - L.offQ), a.code + row0, cb, &full[sq]);
   };
   // A consumer warp calls release(it, s) after its last read of stage s for
   // tile it.  With a producer warp that is an mbarrier arrival; otherwise the
@@ -496,11 +609,23 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
       ptx::prefetch_tmap(&tmV);
       if (ncolQ) ptx::prefetch_tmap(&tmQ);
       if (ncolT) ptx::prefetch_tmap(&tmT);
-      for (int it = 0; it < my_tiles; ++it) {
-        int s, use;
-        stage_of(it, s, use);
-        if (use > 0) ptx::mbar_wait(&empty[s], (use - 1) & 1);
-        issue(it, s);
+      if (dec) {
+        for (int j = 0; j < VLA && j < my_tiles; ++j) issue_v(j, j);
+        for (int it = 0; it < my_tiles; ++it) {
+          const int sq = it % NS, use = it / NS;
+          // tile it - NS released: its basis slot sq and its panel slot, which
+          // panel tile it + VLA (= it - NS + NSV) takes
+          if (use > 0) ptx::mbar_wait(&empty[sq], (use - 1) & 1);
+          issue_q(it, sq);
+          if (it + VLA < my_tiles) issue_v(it + VLA, (it + VLA) % NSV);
+        }
+      } else {
+        for (int it = 0; it < my_tiles; ++it) {
+          int s, use;
+          stage_of(it, s, use);
+          if (use > 0) ptx::mbar_wait(&empty[s], (use - 1) & 1);
+          issue(it, s);
+        }
       }
     }
   } else {
@@ -515,6 +640,29 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
           cfr[ks][nj] = (r < p && c < K) ? -__ldg(a.Cm + r + c * a.ldc) : 0.0;  // L1: one miss per line per SM
         }
     }
+    // tail accumulators (TN > 0): projections tq[mi][c] = sum Q[.][mi*8+g] X[.][8+c],
+    // Gram tg[c] = sum X[.][g] X[.][8+c] and tgg = the lane group's tail x tail pair,
+    // each a partial sum over the rows t4 of the k-steps (reduced over t4 at the end)
+    double tq[TQ ? MQT : 1][TNA];
+    double tg[TG ? TN : 1];
+    double tgg = 0.0;
+    int pa = 0, pb = 0;  // lane group g < NPAIR owns the tail pair (pa <= pb) number g
+    {
+      int e = 0;
+#pragma unroll
+      for (int ca = 0; ca < TN; ++ca)
+#pragma unroll
+        for (int cb = ca; cb < TN; ++cb) {
+          if (e == g) pa = ca, pb = cb;
+          ++e;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < (TQ ? MQT : 1); ++i)
+#pragma unroll
+      for (int c = 0; c < TNA; ++c) tq[i][c] = 0.0;
+#pragma unroll
+    for (int c = 0; c < (TG ? TN : 1); ++c) tg[c] = 0.0;
     double accq[QTX ? MQT : 1][NT][2];
     double accg[GRAM ? NT : 1][NT][2];
     double accs[(SK == SK_GAUSS) ? MST : 1][NT][2];
@@ -594,14 +742,14 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
     } else if (in_trsm_group) {
       // ---------------------------------------------- A: row solves (warps 0-1)
       for (int it = 0; it < my_tiles; ++it) {
-        const int s = it % NS, b = it & 1;
+        const int s = it % NS, sv = it % NSV;
         const long long row0 = (long long)(blockIdx.x + (long long)it * gridDim.x) * T;
         const int valid = (int)(nrows - row0 < T ? nrows - row0 : T);
-        const double* stV = stages + (size_t)s * L.stage + L.offV;
+        const double* stV = slotV(sv);
         double* xt = const_cast<double*>(stV);  // X in place
-        (void)b;
         PP_T0();
-        ptx::mbar_wait(&full[s], (it / NS) & 1);
+        if (dec) ptx::mbar_wait(&fullv[sv], (it / NSV) & 1);
+        else ptx::mbar_wait(&full[s], (it / NS) & 1);
         PP_MARK(8);
         {
           constexpr int GAWX = GAW ? GAW : 1;
@@ -632,8 +780,8 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
         }
         __syncwarp();
         PP_MARK(9);
-        if (lane == 0) ptx::mbar_arrive(&solved[s]);  // X of tile it is in the stage
-        release(it, s);
+        if (lane == 0) ptx::mbar_arrive(&solved[sv]);  // X of tile it is in the stage
+        if (!dec) release(it, s);
         PP_MARK(10);
       }
 #pragma unroll
@@ -643,14 +791,13 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
 #pragma unroll
       for (int e = 0; e < NG; ++e) gacc[e] = 0.0;
       for (int it = 0; it < my_tiles; ++it) {
-        const int s = it % NS, b = it & 1;
+        const int s = it % NS, b = it & 1, sv = it % NSV;
         const long long row0 = (long long)(blockIdx.x + (long long)it * gridDim.x) * T;
         const int valid = (int)(nrows - row0 < T ? nrows - row0 : T);
-        double* st = stages + (size_t)s * L.stage;
-        const double* stV = st + L.offV;
-        const double* stQ = st + L.offQ;
-        const double* stT = st + L.offT;
-        const uint32_t* stC = reinterpret_cast<const uint32_t*>(st + L.offC);
+        const double* stV = slotV(sv);
+        const double* stQ = slotQ(s);
+        const double* stT = stQ + (L.offT - L.offQ);
+        const uint32_t* stC = reinterpret_cast<const uint32_t*>(stQ + (L.offC - L.offQ));
         double* xt = XIN ? const_cast<double*>(stV) : xtile + b * NSUB * KP * S;
 
         // X buffer b was last stored from by tile it - 2: only the group before
@@ -659,7 +806,7 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
         if (!SPLIT && !XIN && STORE && stc < K) ptx::bulk_wait_read1();
         ptx::mbar_wait(&full[s], (it / NS) & 1);
         PP_MARK(0);
-        if (SPLIT) ptx::mbar_wait(&solved[s], (it / NS) & 1);  // solved rows of this tile are in the stage
+        if (SPLIT) ptx::mbar_wait(&solved[sv], (it / NSV) & 1);  // solved rows of this tile are in the stage
         PP_MARK(1);
 
         // ---- U: X = X0 - Q C on tensor cores (rows past the matrix are zero in
@@ -673,30 +820,57 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
           // and the extra registers would spill their sketch accumulators.
           auto upd = [&](auto mq_c) {
             constexpr int MQc = decltype(mq_c)::value;
+            constexpr bool TUc = TU && MQc >= BO_TAIL_UPD_MIN;
+            constexpr int NTD = TUc ? 1 : NT;  // column tiles on DMMA
             for (int rg = gw; rg < T / 8; rg += GW) {
               const int r = rg * 8 + g;
               double av[2 * MQc > 0 ? 2 * MQc : 1];
 #pragma unroll
               for (int ks = 0; ks < 2 * MQc; ++ks) av[ks] = stQ[(ks * 4 + t4) * S + so(r, mq * 8)];
-              double d[NT][2], d1[NT][2];
+              double d[NTD][2], d1[NTD][2], u[TNA];
 #pragma unroll
-              for (int nj = 0; nj < NT; ++nj)
+              for (int nj = 0; nj < NTD; ++nj)
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
                   d[nj][e] = x0[(nj * 8 + 2 * t4 + e) * S + so(r, KP)];
                   d1[nj][e] = 0.0;
                 }
 #pragma unroll
-              for (int ks = 0; ks < 2 * MQc; ++ks)
+              for (int c = 0; c < TNA; ++c) u[c] = 0.0;
 #pragma unroll
-                for (int nj = 0; nj < NT; ++nj) {
+              for (int ks = 0; ks < 2 * MQc; ++ks) {
+#pragma unroll
+                for (int nj = 0; nj < NTD; ++nj) {
                   if (SPLIT && (ks & 1)) ptx::dmma(d1[nj][0], d1[nj][1], av[ks], cfr[ks][nj]);
                   else ptx::dmma(d[nj][0], d[nj][1], av[ks], cfr[ks][nj]);
                 }
+                if constexpr (TUc) {
+                  const double* cr = ctls + (ks * 4 + t4) * 4;
+                  const double2 c01 = *reinterpret_cast<const double2*>(cr);
+                  const double ct[3] = {c01.x, c01.y, TN > 2 ? cr[2] : 0.0};
 #pragma unroll
-              for (int nj = 0; nj < NT; ++nj)
+                  for (int c = 0; c < TN; ++c) u[c] = fma(av[ks], ct[c], u[c]);
+                }
+              }
+#pragma unroll
+              for (int nj = 0; nj < NTD; ++nj)
 #pragma unroll
                 for (int e = 0; e < 2; ++e) xt[(nj * 8 + 2 * t4 + e) * S + so(r, KP)] = SPLIT ? d[nj][e] + d1[nj][e] : d[nj][e];
+              if constexpr (TUc) {
+                // sum the tail partials over the four t4 lanes of row g; lane t4 < TN
+                // then writes column 8 + t4 of that row
+                double ux = 0.0;
+#pragma unroll
+                for (int c = 0; c < TN; ++c) {
+                  u[c] += __shfl_xor_sync(0xffffffffu, u[c], 1);
+                  u[c] += __shfl_xor_sync(0xffffffffu, u[c], 2);
+                  if (c == t4) ux = u[c];
+                }
+                if (t4 < TN) {
+                  double* xp = xt + (8 + t4) * S + so(r, KP);
+                  *xp = x0[(8 + t4) * S + so(r, KP)] + ux;
+                }
+              }
             }
           };
           switch (mq) {
@@ -755,12 +929,19 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
           auto contract = [&](auto m_c) {
             constexpr int M = decltype(m_c)::value;          // Q or Theta tiles (may be 0)
             constexpr int MQc = QTX ? M : 0, MSc = (SK == SK_GAUSS) ? M : 0;
-            double bx[2][NT], aq[2][MQc > 0 ? MQc : 1], at[2][MSc > 0 ? MSc : 1];
+            constexpr bool TQc = TQ && M >= BO_TAIL_QTX_MIN;
+            constexpr int NTQ = TQc ? 1 : NT;  // projection column tiles on DMMA
+            // column tiles of X fragments needed, and whether the tail columns are loaded
+            constexpr int NTD = ((QTX && !TQc) || (GRAM && !TG) || SK == SK_GAUSS) ? NT : 1;
+            constexpr int XTN = (TQc || TG) ? TN : 0;
+            double bx[2][NTD], xtl[2][TNA], aq[2][MQc > 0 ? MQc : 1], at[2][MSc > 0 ? MSc : 1];
             auto load = [&](int ks, auto slot_c) {
               constexpr int slot = decltype(slot_c)::value;  // register-resident fragment sets
               const int r = ks * 4 + t4;
 #pragma unroll
-              for (int nj = 0; nj < NT; ++nj) bx[slot][nj] = X[(nj * 8 + g) * S + so(r, KP)];
+              for (int nj = 0; nj < NTD; ++nj) bx[slot][nj] = X[(nj * 8 + g) * S + so(r, KP)];
+#pragma unroll
+              for (int c = 0; c < XTN; ++c) xtl[slot][c] = X[(8 + c) * S + so(r, KP)];  // 4 addresses per warp
               if (QTX) {
 #pragma unroll
                 for (int mi = 0; mi < MQc; ++mi) aq[slot][mi] = stQ[(mi * 8 + g) * S + so(r, mq * 8)];
@@ -774,23 +955,39 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
               constexpr int slot = decltype(slot_c)::value;
               if (QTX) {
 #pragma unroll
-                for (int mi = 0; mi < MQc; ++mi)
+                for (int mi = 0; mi < MQc; ++mi) {
 #pragma unroll
-                  for (int nj = 0; nj < NT; ++nj)
+                  for (int nj = 0; nj < NTQ; ++nj)
                     ptx::dmma(accq[mi][nj][0], accq[mi][nj][1], aq[slot][mi], bx[slot][nj]);
+                  if constexpr (TQc) {
+#pragma unroll
+                    for (int c = 0; c < TN; ++c) tq[mi][c] = fma(aq[slot][mi], xtl[slot][c], tq[mi][c]);
+                  }
+                }
               }
               if (GRAM) {
 #pragma unroll
-                for (int mi = 0; mi < NT; ++mi)
+                for (int mi = 0; mi < NTG; ++mi)
 #pragma unroll
-                  for (int nj = 0; nj < NT; ++nj)
+                  for (int nj = 0; nj < NTG; ++nj)
                     if (mi <= nj) ptx::dmma(accg[mi][nj][0], accg[mi][nj][1], bx[slot][mi], bx[slot][nj]);
+                if constexpr (TG) {
+#pragma unroll
+                  for (int c = 0; c < TN; ++c) tg[c] = fma(bx[slot][0], xtl[slot][c], tg[c]);
+                  double xa = xtl[slot][0], xb = xtl[slot][0];
+#pragma unroll
+                  for (int c = 1; c < TN; ++c) {
+                    xa = pa == c ? xtl[slot][c] : xa;
+                    xb = pb == c ? xtl[slot][c] : xb;
+                  }
+                  tgg = fma(xa, xb, tgg);
+                }
               }
               if (SK == SK_GAUSS) {
 #pragma unroll
                 for (int mi = 0; mi < MSc; ++mi)
 #pragma unroll
-                  for (int nj = 0; nj < NT; ++nj)
+                  for (int nj = 0; nj < NTD; ++nj)
                     ptx::dmma(accs[mi][nj][0], accs[mi][nj][1], at[slot][mi], bx[slot][nj]);
               }
             };
@@ -872,6 +1069,27 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
     const int dm_len = a.dm_len;
     for (int e = lane; e < dm_len; e += 32) red[warp * dm_len + e] = 0.0;
     __syncwarp();
+    if constexpr (TQ || TG) {
+      // tail partial sums over the t4 lanes (fixed butterfly order)
+#pragma unroll
+      for (int c = 0; c < TN; ++c) {
+        if (TQ) {
+#pragma unroll
+          for (int mi = 0; mi < MQT; ++mi) {
+            tq[mi][c] += __shfl_xor_sync(0xffffffffu, tq[mi][c], 1);
+            tq[mi][c] += __shfl_xor_sync(0xffffffffu, tq[mi][c], 2);
+          }
+        }
+        if (TG) {
+          tg[c] += __shfl_xor_sync(0xffffffffu, tg[c], 1);
+          tg[c] += __shfl_xor_sync(0xffffffffu, tg[c], 2);
+        }
+      }
+      if (TG) {
+        tgg += __shfl_xor_sync(0xffffffffu, tgg, 1);
+        tgg += __shfl_xor_sync(0xffffffffu, tgg, 2);
+      }
+    }
     if (QTX) {
 #pragma unroll
       for (int mi = 0; mi < MQT; ++mi)
@@ -882,6 +1100,18 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
             const int i = mi * 8 + g, j = nj * 8 + 2 * t4 + e;
             if (i < a.ld_q && j < 16) red[warp * dm_len + a.off_q + i + j * a.ld_q] = accq[mi][nj][e];
           }
+      if constexpr (TQ) {
+        // this launch's Q-tile count chose either the DMMA tile or the tail: the
+        // other one is all zeros, so the sum is exact
+        __syncwarp();
+#pragma unroll
+        for (int mi = 0; mi < MQT; ++mi)
+#pragma unroll
+          for (int c = 0; c < TN; ++c) {
+            const int i = mi * 8 + g;
+            if (t4 == 0 && i < a.ld_q) red[warp * dm_len + a.off_q + i + (8 + c) * a.ld_q] += tq[mi][c];
+          }
+      }
     }
     if (ROWG) {
       if (lane == 0) {
@@ -897,9 +1127,9 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
       }
     } else if (GRAM) {
 #pragma unroll
-      for (int mi = 0; mi < NT; ++mi)
+      for (int mi = 0; mi < NTG; ++mi)
 #pragma unroll
-        for (int nj = 0; nj < NT; ++nj)
+        for (int nj = 0; nj < NTG; ++nj)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int i = mi * 8 + g, j = nj * 8 + 2 * t4 + e;
@@ -908,6 +1138,19 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
               if (mi < nj) red[warp * dm_len + a.off_g + j + i * 16] = accg[mi][nj][e];
             }
           }
+      if constexpr (TG) {
+        if (t4 == 0) {
+#pragma unroll
+          for (int c = 0; c < TN; ++c) {
+            red[warp * dm_len + a.off_g + g + (8 + c) * 16] = tg[c];
+            red[warp * dm_len + a.off_g + (8 + c) + g * 16] = tg[c];
+          }
+          if (g < NPAIR) {
+            red[warp * dm_len + a.off_g + (8 + pa) + (8 + pb) * 16] = tgg;
+            red[warp * dm_len + a.off_g + (8 + pb) + (8 + pa) * 16] = tgg;
+          }
+        }
+      }
     }
     if (SK == SK_GAUSS) {
 #pragma unroll
