@@ -453,7 +453,7 @@ int run_pass(bo_ctx ctx, PassReq& r, bo_status* st) {
     if (ki.qtx) {
       q.fin.q_row_off = c0;
       if (!last) {
-        q.kind = ki.npre == 2 ? PK_P2_QTX : PK_QTX;
+        q.kind = ki.npre == 2 ? PK_P2_QTX : ki.npre == 1 ? PK_P1_QTX : PK_QTX;
         q.fin.ops = FIN_COPY_Q;
       }
     } else {
@@ -464,11 +464,11 @@ int run_pass(bo_ctx ctx, PassReq& r, bo_status* st) {
         q.Rpre0 = q.Rpre1 = nullptr;
       }
       if (!last) {
-        q.kind = (c0 == 0 && ki.npre == 2) ? PK_P2_UPD_ST : PK_UPD_ST;
+        q.kind = (c0 == 0 && ki.npre == 2) ? PK_P2_UPD_ST : (c0 == 0 && ki.npre == 1) ? PK_P1_UPD_ST : PK_UPD_ST;
         q.fin.ops = 0;
         q.sk = nullptr;
-      } else if (c0 > 0 && ki.npre == 2) {
-        q.kind = PK_UPD_GRAM_ST;  // the only pre-solve update kind (P2_UPD_GRAM_ST) minus its solve
+      } else if (c0 > 0 && ki.npre > 0) {
+        q.kind = PK_UPD_GRAM_ST;  // the pre-solve update kinds (P1/P2_UPD_GRAM_ST) minus their solve
       }
       if (!r.out) return set_st(st, BO_INVALID, 0, 0.0, "chunked update needs an output buffer");
     }
@@ -1206,6 +1206,10 @@ int dev_intra(bo_ctx ctx, const double* v, uint64_t ldv, int K, int intra, bo_sk
   g2.fin.rjj = T_(ctx, OFF_RIN);
   TRY(run_pass(ctx, g2, st));
   if (q) {
+    // Two solves here, not one with Rin = R2 R1 (as bcgs2's P4 / P5 do): this
+    // Q is final, and the second solve is what re-orthogonalises it (measured:
+    // the product factor gave ||I - Q^T Q|| 1.3e-11 against the reference's
+    // 1.7e-13 for CholQR2 at cond 1e6)
     PassReq w{};
     w.kind = PK_P2_ST;
     w.K = K;
@@ -1791,32 +1795,42 @@ extern "C" int bo_bcgs2_enqueue(bo_basis b, const double* v, uint64_t ldv, uint6
   r3.fin.Rin = T_(ctx, OFF_R1);
   r3.fin.rjj = T_(ctx, OFF_RIN);
   TRY(run_pass(ctx, r3, st));
-  // P4: Qhat = Vhat R1^-1 R2^-1 ; C2 = Q^T Qhat
+  // P4: Qhat = Vhat R1^-1 R2^-1 ; C2 = Q^T Qhat.  With the product factor
+  // (default) the row solve is Vhat Rin^-1, Rin = R2 R1 (P3's FIN_MULT):
+  // one triangular solve per row instead of two.  The reference solves twice
+  // (intra_orth.cpp:28-39); the single solve differs from it by rounding
+  // amplified by cond(R1) (the problem's own sensitivity; P5/P6 re-
+  // orthogonalise), and halves the FP64 solve work of the two solve warps,
+  // which share their sub-partitions' FP64 pipe with the DMMA contraction.
+  static const bool pre_product = [] {
+    const char* e = getenv("BO_PRE_PRODUCT");
+    return e ? atoi(e) != 0 : true;
+  }();
   PassReq r4{};
-  r4.kind = PK_P2_QTX;
+  r4.kind = pre_product ? PK_P1_QTX : PK_P2_QTX;
   r4.K = K;
   r4.V = vhat;
   r4.ldv = ctx->ld;
   r4.Q = Q;
   r4.ldq = ctx->ld;
   r4.p = p;
-  r4.Rpre0 = T_(ctx, OFF_R1);
-  r4.Rpre1 = T_(ctx, OFF_R2);
+  r4.Rpre0 = pre_product ? T_(ctx, OFF_RIN) : T_(ctx, OFF_R1);
+  r4.Rpre1 = pre_product ? nullptr : T_(ctx, OFF_R2);
   r4.pass_id = 4;
   r4.fin.ops = FIN_COPY_Q;
   r4.fin.Cq = T_(ctx, OFF_C2);
   TRY(run_pass(ctx, r4, st));
   // P5: Z = Qhat - Q C2 (in place over Vhat) ; G3 = Z^T Z -> R3 ; coeffs, rjj
   PassReq r5{};
-  r5.kind = PK_P2_UPD_GRAM_ST;
+  r5.kind = pre_product ? PK_P1_UPD_GRAM_ST : PK_P2_UPD_GRAM_ST;
   r5.K = K;
   r5.V = vhat;
   r5.ldv = ctx->ld;
   r5.Q = Q;
   r5.ldq = ctx->ld;
   r5.p = p;
-  r5.Rpre0 = T_(ctx, OFF_R1);
-  r5.Rpre1 = T_(ctx, OFF_R2);
+  r5.Rpre0 = pre_product ? T_(ctx, OFF_RIN) : T_(ctx, OFF_R1);
+  r5.Rpre1 = pre_product ? nullptr : T_(ctx, OFF_R2);
   r5.Cm = T_(ctx, OFF_C2);
   r5.out = vhat;
   r5.ldo = ctx->ld;

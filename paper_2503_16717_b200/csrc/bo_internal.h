@@ -181,7 +181,10 @@ namespace host {
   X(P1_ST, 1, false, 0, false, false, SK_NONE, true)                   \
   X(P2_ST, 2, false, 0, false, false, SK_NONE, true)                    \
   X(UPD_POST_ST, 0, true, 1, false, false, SK_NONE, true)              \
-  X(P2_UPD_ST, 2, true, 0, false, false, SK_NONE, true)
+  X(P2_UPD_ST, 2, true, 0, false, false, SK_NONE, true)                \
+  X(P1_QTX, 1, false, 0, true, false, SK_NONE, false)                  \
+  X(P1_UPD_GRAM_ST, 1, true, 0, false, true, SK_NONE, true)            \
+  X(P1_UPD_ST, 1, true, 0, false, false, SK_NONE, true)
 
 enum PassKind {
 #define X(nm, a, b, c, d, e, f, g) PK_##nm,

@@ -7,5 +7,5 @@ mkdir -p $OUT
 for spec in "$@"; do
   label=${spec%%:*}; envs=${spec#*:}
   (env $envs timeout 300 python scripts/prof_passes.py > $OUT/passes_$label.txt 2>&1)
-  echo "== $label ($envs)"; grep -E "P2_QTX|P2_UPD_GRAM|P1_GRAM|P1_ST|sum of" $OUT/passes_$label.txt
+  echo "== $label ($envs)"; grep -E "P[12]_QTX|P[12]_UPD_GRAM|sum of" $OUT/passes_$label.txt
 done
