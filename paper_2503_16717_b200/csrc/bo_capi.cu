@@ -323,6 +323,15 @@ int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st) {
   a.nstages = NS;
   a.nstages_v = NSV;
   {
+    // one solve warp for single-solve projection passes with a wide basis
+    // block (bo_pass.cuh gaw; measured on the C2 sequence, scripts/ab_tail.sh)
+    static const int gaw_minp = [] {
+      const char* e = getenv("BO_GAW1_MINP");
+      return e ? atoi(e) : 25;
+    }();
+    a.gaw = (ki.npre == 1 && ki.qtx && T <= 128 && gaw_minp > 0 && r.p >= gaw_minp) ? 1 : 0;
+  }
+  {
     // bytes to keep in flight per SM (L2 prefetch + ring): loaded HBM latency
     // x per-SM bandwidth with margin (~5 us x 44 GB/s)
     static const long long pf_kb = [] {

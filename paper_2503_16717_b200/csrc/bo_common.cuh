@@ -171,6 +171,7 @@ struct PassArgs {
   unsigned* counter;
   int part_len, off_q, ld_q, off_g, off_s, ld_s;
   int nstages;
+  int gaw;                 // solve warps of a pre-solve projection pass (0: the build's default)
   int nstages_v;           // panel-ring depth of the decoupled pre-solve passes (bo_pass.cuh DEC)
   int prefetch_tiles;      // L2 prefetch lookahead beyond the stage ring (tiles)
   int region0_dbl;         // doubles of shared region 0 (stage ring / reduction / finalize scratch)

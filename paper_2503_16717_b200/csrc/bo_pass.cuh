@@ -342,9 +342,15 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
   // sub-partition) was 3% slower over the C2 sequence, since the update is
   // bound by the shared FP64 pipe, not by which sub-partition issues it.
   constexpr int GAW0 = (NPRE > 0 && QTX) ? BO_GAW_QTX : (NPRE > 0 && UPD) ? BO_GAW_UPD : BO_GAW;
-  constexpr int GAW = SPLIT ? (GAW0 > 0 ? GAW0 : NW - 4) : 0;
-  constexpr int GW = NW - GAW;             // warps of the U/S/R group
-  constexpr int GT = GW * 32;
+  constexpr int GAWR = SPLIT ? (GAW0 > 0 ? GAW0 : NW - 4) : 0;
+  constexpr int GAW = (SPLIT && GAWR * 128 < T) ? T / 128 : GAWR;  // at most four rows per solve thread
+  // Solve warps of this launch.  The pre-solve projection passes (one solve,
+  // QTX) take a.gaw = 1 where the basis block is wide (host: p >= 25), which
+  // gives the contraction a sixth warp (measured P1_QTX p = 55 739 -> 667 us,
+  // but 400 -> 466 us at p = 11, where one warp's solve is the bound).
+  const int gaw = (SPLIT && QTX && a.gaw > 0 && a.gaw < GAW && a.gaw * 128 >= T) ? a.gaw : GAW;
+  const int GW = NW - gaw;                 // warps of the U/S/R group
+  const int GT = GW * 32;
   constexpr int GBAR = SPLIT ? 6 : 1;      // named barrier of the U/S/R group
   constexpr bool XT = (NPRE > 0) || UPD || (NPOST > 0);  // X lives in the X tile
   // X is computed in place in the stage's V block (each row / row group is
@@ -446,7 +452,7 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
       else reinterpret_cast<unsigned*>(&empty[s])[0] = 0u;  // arrival counter
     }
     for (int s = 0; s < NSV; ++s) {
-      if (SPLIT) ptx::mbar_init(&solved[s], GAW);
+      if (SPLIT) ptx::mbar_init(&solved[s], gaw);
       if (dec) ptx::mbar_init(&fullv[s], 1);
     }
     ptx::fence_mbar_init();
@@ -679,8 +685,8 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
 #pragma unroll
       for (int j = 0; j < NT; ++j) accs[i][j][0] = accs[i][j][1] = 0.0;
 
-    const bool in_trsm_group = SPLIT && !ROWG && warp < GAW;
-    const int gw = warp - GAW;  // warp index within the U/S/R group
+    const bool in_trsm_group = SPLIT && !ROWG && warp < gaw;
+    const int gw = warp - gaw;  // warp index within the U/S/R group
     const int gtid = gw * 32 + lane;
     // bulk stores: column c is issued by lane c / GW of group warp c % GW, so
     // the issue cost (proxy fence + one bulk copy per column and sub-tile) is
@@ -751,8 +757,8 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
         if (dec) ptx::mbar_wait(&fullv[sv], (it / NSV) & 1);
         else ptx::mbar_wait(&full[s], (it / NS) & 1);
         PP_MARK(8);
-        {
-          constexpr int GAWX = GAW ? GAW : 1;
+        auto solve = [&](auto gaw_c) {
+          constexpr int GAWX = decltype(gaw_c)::value;
           constexpr int RPT = (T + GAWX * 32 - 1) / (GAWX * 32);  // rows per thread
           double x[RPT][kMaxK];
 #pragma unroll
@@ -777,6 +783,13 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
                 if (c < K) xt[c * S + so(r, KP)] = (r < valid) ? x[q][c] : 0.0;
             }
           }
+        };
+        constexpr int GAWC = GAW ? GAW : 1;
+        if constexpr (QTX && GAWC > 1 && T <= 128) {
+          if (gaw == 1) solve(std::integral_constant<int, 1>{});
+          else solve(std::integral_constant<int, GAWC>{});
+        } else {
+          solve(std::integral_constant<int, GAWC>{});
         }
         __syncwarp();
         PP_MARK(9);
