@@ -382,8 +382,10 @@ def main():
         for i, vp in enumerate(panels):
             if i == len(panels) - 1:
                 torch.cuda.nvtx.range_push("last")
+            if i == 1:
+                torch.cuda.nvtx.range_push("p11")  # the p = 11 call
             P.bcgs2(store, vp, intra, theta)
-            if i == len(panels) - 1:
+            if i == len(panels) - 1 or i == 1:
                 torch.cuda.nvtx.range_pop()
         torch.cuda.nvtx.range_pop()
         ctx.synchronize()

@@ -314,6 +314,25 @@ __device__ __forceinline__ void row_trsm_n(double (&x)[NR][kMaxK], const double*
   }
 }
 
+// slot = i % n and phase = (i / n) & 1 of a ring position i, advanced without
+// the integer division (~25 instructions each for a runtime n: the four per
+// tile of the consumer loops were 16% of the stall samples of a p = 11
+// projection pass)
+struct RingCursor {
+  int slot = 0, n;
+  uint32_t phase = 0;
+  __device__ explicit RingCursor(int n_, int start = 0) : n(n_) {
+    slot = start;
+    while (slot >= n) slot -= n, phase ^= 1u;
+  }
+  __device__ __forceinline__ void next() {
+    if (++slot == n) {
+      slot = 0;
+      phase ^= 1u;
+    }
+  }
+};
+
 // ---------------------------------------------------------------------------
 // the pass kernel
 // ---------------------------------------------------------------------------
@@ -617,13 +636,19 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
       if (ncolT) ptx::prefetch_tmap(&tmT);
       if (dec) {
         for (int j = 0; j < VLA && j < my_tiles; ++j) issue_v(j, j);
-        for (int it = 0; it < my_tiles; ++it) {
-          const int sq = it % NS, use = it / NS;
-          // tile it - NS released: its basis slot sq and its panel slot, which
+        RingCursor cq(NS), cv(NSV, VLA);
+        for (int it = 0; it < my_tiles; ++it, cq.next(), cv.next()) {
+          // tile it - NS released: its basis slot and its panel slot, which
           // panel tile it + VLA (= it - NS + NSV) takes
-          if (use > 0) ptx::mbar_wait(&empty[sq], (use - 1) & 1);
-          issue_q(it, sq);
-          if (it + VLA < my_tiles) issue_v(it + VLA, (it + VLA) % NSV);
+          if (it >= NS) ptx::mbar_wait(&empty[cq.slot], cq.phase ^ 1u);
+          issue_q(it, cq.slot);
+          if (it + VLA < my_tiles) issue_v(it + VLA, cv.slot);
+        }
+      } else if (!ROWG) {
+        RingCursor c(NS);
+        for (int it = 0; it < my_tiles; ++it, c.next()) {
+          if (it >= NS) ptx::mbar_wait(&empty[c.slot], c.phase ^ 1u);
+          issue(it, c.slot);
         }
       } else {
         for (int it = 0; it < my_tiles; ++it) {
@@ -707,12 +732,13 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
       // (q < 4): four independent rows per solve step (ILP, and one shared-
       // memory read of each R entry per four FMAs)
       constexpr int RQ = KC > 8 ? 1 : 2;  // rows per thread per step (register budget: 168 with 9 warps)
-      for (int j = 0, it = warp; it < my_tiles; ++j, it += NW) {
-        const int s = warp + NW * (j % nsub);
+      RingCursor cr(nsub);
+      for (int j = 0, it = warp; it < my_tiles; ++j, it += NW, cr.next()) {
+        const int s = warp + NW * cr.slot;
         const long long row0 = (long long)(blockIdx.x + (long long)it * gridDim.x) * T;
         const int valid = (int)(nrows - row0 < T ? nrows - row0 : T);
         const double* stV = stages + (size_t)s * L.stage + L.offV;
-        ptx::mbar_wait(&full[s], (j / nsub) & 1);
+        ptx::mbar_wait(&full[s], cr.phase);
         for (int h = 0; h < T / (32 * RQ); ++h) {
           // keep the R entries in shared memory (re-read per step) rather than
           // hoisted into registers next to the K(K+1)/2 accumulators
@@ -747,15 +773,16 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
       }
     } else if (in_trsm_group) {
       // ---------------------------------------------- A: row solves (warps 0-1)
-      for (int it = 0; it < my_tiles; ++it) {
-        const int s = it % NS, sv = it % NSV;
+      RingCursor cs(NS), csv(NSV);
+      for (int it = 0; it < my_tiles; ++it, cs.next(), csv.next()) {
+        const int s = cs.slot, sv = csv.slot;
         const long long row0 = (long long)(blockIdx.x + (long long)it * gridDim.x) * T;
         const int valid = (int)(nrows - row0 < T ? nrows - row0 : T);
         const double* stV = slotV(sv);
         double* xt = const_cast<double*>(stV);  // X in place
         PP_T0();
-        if (dec) ptx::mbar_wait(&fullv[sv], (it / NSV) & 1);
-        else ptx::mbar_wait(&full[s], (it / NS) & 1);
+        if (dec) ptx::mbar_wait(&fullv[sv], csv.phase);
+        else ptx::mbar_wait(&full[s], cs.phase);
         PP_MARK(8);
         auto solve = [&](auto gaw_c) {
           constexpr int GAWX = decltype(gaw_c)::value;
@@ -803,8 +830,9 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
       // ------------------------------------------- U / A' / S / R group
 #pragma unroll
       for (int e = 0; e < NG; ++e) gacc[e] = 0.0;
-      for (int it = 0; it < my_tiles; ++it) {
-        const int s = it % NS, b = it & 1, sv = it % NSV;
+      RingCursor cs(NS), csv(NSV);
+      for (int it = 0; it < my_tiles; ++it, cs.next(), csv.next()) {
+        const int s = cs.slot, b = it & 1, sv = csv.slot;
         const long long row0 = (long long)(blockIdx.x + (long long)it * gridDim.x) * T;
         const int valid = (int)(nrows - row0 < T ? nrows - row0 : T);
         const double* stV = slotV(sv);
@@ -817,9 +845,9 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
         // the most recent one (tile it - 1, other buffer) has to be drained
         PP_T0();
         if (!SPLIT && !XIN && STORE && stc < K) ptx::bulk_wait_read1();
-        ptx::mbar_wait(&full[s], (it / NS) & 1);
+        ptx::mbar_wait(&full[s], cs.phase);
         PP_MARK(0);
-        if (SPLIT) ptx::mbar_wait(&solved[sv], (it / NSV) & 1);  // solved rows of this tile are in the stage
+        if (SPLIT) ptx::mbar_wait(&solved[sv], csv.phase);  // solved rows of this tile are in the stage
         PP_MARK(1);
 
         // ---- U: X = X0 - Q C on tensor cores (rows past the matrix are zero in
