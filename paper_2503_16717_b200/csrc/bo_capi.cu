@@ -330,6 +330,14 @@ int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st) {
       return e ? atoi(e) : 25;
     }();
     a.gaw = (ki.npre == 1 && ki.qtx && T <= 128 && gaw_minp > 0 && r.p >= gaw_minp) ? 1 : 0;
+    // narrow pre-solve projections: BO_QTX_GW_SMALLP=n contracts on n warps
+    // (measured slower: p = 11 397 / 441 / 514 us with 5 / 4 / 3 warps, so the
+    // pass is bound by latency, not by two warps sharing a DMMA pipe; off)
+    static const int gw_small = [] {
+      const char* e = getenv("BO_QTX_GW_SMALLP");
+      return e ? atoi(e) : 0;
+    }();
+    a.gw_active = (ki.npre > 0 && ki.qtx && a.gaw == 0 && gw_small > 0 && r.p < gaw_minp) ? gw_small : 0;
   }
   {
     // bytes to keep in flight per SM (L2 prefetch + ring): loaded HBM latency

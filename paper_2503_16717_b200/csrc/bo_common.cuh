@@ -172,6 +172,7 @@ struct PassArgs {
   int part_len, off_q, ld_q, off_g, off_s, ld_s;
   int nstages;
   int gaw;                 // solve warps of a pre-solve projection pass (0: the build's default)
+  int gw_active;           // U/S/R warps of a pre-solve projection pass (0: all the others)
   int nstages_v;           // panel-ring depth of the decoupled pre-solve passes (bo_pass.cuh DEC)
   int prefetch_tiles;      // L2 prefetch lookahead beyond the stage ring (tiles)
   int region0_dbl;         // doubles of shared region 0 (stage ring / reduction / finalize scratch)

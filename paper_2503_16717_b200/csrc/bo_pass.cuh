@@ -368,7 +368,9 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
   // gives the contraction a sixth warp (measured P1_QTX p = 55 739 -> 667 us,
   // but 400 -> 466 us at p = 11, where one warp's solve is the bound).
   const int gaw = (SPLIT && QTX && a.gaw > 0 && a.gaw < GAW && a.gaw * 128 >= T) ? a.gaw : GAW;
-  const int GW = NW - gaw;                 // warps of the U/S/R group
+  // warps of the U/S/R group.  a.gw_active < NW - gaw leaves the rest idle
+  // (diagnostic: BO_QTX_GW_SMALLP; fewer contraction warps measured slower)
+  const int GW = (SPLIT && QTX && a.gw_active > 0 && a.gw_active < NW - gaw) ? a.gw_active : NW - gaw;
   const int GT = GW * 32;
   constexpr int GBAR = SPLIT ? 6 : 1;      // named barrier of the U/S/R group
   constexpr bool XT = (NPRE > 0) || UPD || (NPOST > 0);  // X lives in the X tile
@@ -467,7 +469,7 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
       ptx::mbar_init(&full[s], 1);
       // DEC: only the U/S/R group releases (the solve warps are done with a
       // tile before the group starts it)
-      if (BO_PRODUCER_WARP) ptx::mbar_init(&empty[s], ROWG ? 1 : (dec ? GW : NW));
+      if (BO_PRODUCER_WARP) ptx::mbar_init(&empty[s], ROWG ? 1 : (dec ? GW : gaw + GW));
       else reinterpret_cast<unsigned*>(&empty[s])[0] = 0u;  // arrival counter
     }
     for (int s = 0; s < NSV; ++s) {
@@ -831,7 +833,7 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
 #pragma unroll
       for (int e = 0; e < NG; ++e) gacc[e] = 0.0;
       RingCursor cs(NS), csv(NSV);
-      for (int it = 0; it < my_tiles; ++it, cs.next(), csv.next()) {
+      for (int it = 0; it < (gw < GW ? my_tiles : 0); ++it, cs.next(), csv.next()) {
         const int s = cs.slot, b = it & 1, sv = csv.slot;
         const long long row0 = (long long)(blockIdx.x + (long long)it * gridDim.x) * T;
         const int valid = (int)(nrows - row0 < T ? nrows - row0 : T);
