@@ -234,12 +234,8 @@ BO_DDM_FN double log_fast(double x, bool* ok) {
   return r.hi;
 }
 
-BO_DDM_FN void sincos_fast(double a, double* sn, double* cs, bool* ok) {
-  const double kd = RINT(M(a, kTwoOverPi));
-  const int k = (int)kd;
-  DD r = add(DD{a, 0.0}, neg(two_prod(kd, kPio2_1)));  // accurate adds: r may be ~1e-16 (a near k pi/2)
-  r = add(r, neg(two_prod(kd, kPio2_2)));
-  r = add_d(r, -M(kd, kPio2_3));
+// sin / cos of the reduced argument r = a - k pi/2 (a double-double), fast path
+BO_DDM_FN void sincos_fast_reduced(DD r, int k, double* sn, double* cs, bool* ok) {
   const double jd = RINT(M(r.hi, 64.0));
   const int j = (int)jd;
   const DD dl = two_sum(S(r.hi, M(jd, 0x1p-6)), r.lo);
@@ -296,6 +292,40 @@ BO_DDM_FN void sincos_fast(double a, double* sn, double* cs, bool* ok) {
   }
 }
 
+BO_DDM_FN void sincos_fast(double a, double* sn, double* cs, bool* ok) {
+  const double kd = RINT(M(a, kTwoOverPi));
+  DD r = add(DD{a, 0.0}, neg(two_prod(kd, kPio2_1)));  // accurate adds: r may be ~1e-16 (a near k pi/2)
+  r = add(r, neg(two_prod(kd, kPio2_2)));
+  r = add_d(r, -M(kd, kPio2_3));
+  sincos_fast_reduced(r, (int)kd, sn, cs, ok);
+}
+
+// The Box-Muller angle a = fl(C u2), C = fl(2 pi), u2 = i 2^-53 in [0, 1)
+// (rng.hpp:37-49), reduced without a three-part pi/2.  With kd = rint(4 u2)
+// and d = u2 - kd/4 (exact: both are multiples of 2^-53 and |d| <= 1/8),
+//   a = C u2 + e,  e = -(C u2 - a) = -fma(C, u2, -a)   (exact),
+//   r = a - kd pi/2 = C d + e + kd (C - 2 pi)/4,
+// with C d exact as two_prod(C, d) and (C - 2 pi)/4 as a double-double
+// (kBmQ): two exact two_sums and three small terms, error below 2^-100 |r|
+// (|r| >= 6e-17 unless a = 0, where r = 0 exactly), where the general
+// reduction spends three double-double additions.  Same k as the general
+// reduction up to ties, so the results are the same correctly rounded values.
+constexpr double kBmC = 6.283185307179586476925286766559;
+constexpr double kBmQHi = -0x1.1a62633145c07p-54, kBmQLo = 0x1.f1976b7ed8fbcp-110;  // (kBmC - 2 pi) / 4
+BO_DDM_FN void sincos_bm_fast(double u2, double* sn, double* cs, bool* ok) {
+  const double a = M(kBmC, u2);
+  const double kd = RINT(M(u2, 4.0));
+  const double d = S(u2, M(kd, 0.25));
+  const double e = -F(kBmC, u2, -a);
+  const DD p = two_prod(kBmC, d);
+  const DD s1 = two_sum(p.hi, e);
+  const DD s2 = two_sum(s1.hi, M(kd, kBmQHi));  // kd <= 4: the product is exact
+  double lo = A(s1.lo, s2.lo);
+  lo = A(lo, p.lo);
+  lo = F(kd, kBmQLo, lo);
+  sincos_fast_reduced(quick_two_sum(s2.hi, lo), (int)kd, sn, cs, ok);
+}
+
 // correctly rounded log / sincos: fast path, full precision where the fast
 // result's rounding is not certain
 BO_DDM_FN double log_cr(double x) {
@@ -307,6 +337,12 @@ BO_DDM_FN void sincos_cr(double a, double* sn, double* cs) {
   bool ok;
   sincos_fast(a, sn, cs, &ok);
   if (!ok) sincos_rn(a, sn, cs);
+}
+// sin / cos of the Box-Muller angle fl(kBmC u2), correctly rounded
+BO_DDM_FN void sincos_bm_cr(double u2, double* sn, double* cs) {
+  bool ok;
+  sincos_bm_fast(u2, sn, cs, &ok);
+  if (!ok) sincos_rn(M(kBmC, u2), sn, cs);
 }
 
 }  // namespace ddm

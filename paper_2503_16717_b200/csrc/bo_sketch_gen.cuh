@@ -80,9 +80,8 @@ __device__ __forceinline__ void gen_transform(const GenArgs& a, const uint64_t* 
     // correctly rounded log / sin / cos (bo_ddmath.cuh): the only differences
     // from the reference left are glibc's own misroundings (~0.1 % of inputs)
     const double rr = sqrt(tiny::mul(-2.0, ddm::log_cr(u1)));
-    const double ang = tiny::mul(6.283185307179586476925286766559, u2);
     double sn, cs;
-    ddm::sincos_cr(ang, &sn, &cs);
+    ddm::sincos_bm_cr(u2, &sn, &cs);  // of ang = fl(2 pi u2), reduced through u2 (bo_ddmath.cuh)
     const double v0 = tiny::mul(a.scale, tiny::mul(rr, cs));
     const double v1 = tiny::mul(a.scale, tiny::mul(rr, sn));
     uint64_t c1 = col, r1 = row + 1;

@@ -27,6 +27,18 @@ void ddm_cr_n(const double* x, const double* a, double* lg, double* s, double* c
   }
 }
 void ddm_sincos(double a, double* s, double* c) { bo::ddm::sincos_rn(a, s, c); }
+// the Box-Muller-specific reduction (device generator): fast path with its
+// certainty flag, and the combined function, both from u2
+void ddm_bm_fast_n(const double* u2, double* s, double* c, unsigned char* ok, long n) {
+  for (long i = 0; i < n; ++i) {
+    bool o;
+    bo::ddm::sincos_bm_fast(u2[i], s + i, c + i, &o);
+    ok[i] = o;
+  }
+}
+void ddm_bm_cr_n(const double* u2, double* s, double* c, long n) {
+  for (long i = 0; i < n; ++i) bo::ddm::sincos_bm_cr(u2[i], s + i, c + i);
+}
 void ddm_log_n(const double* x, double* y, long n) {
   for (long i = 0; i < n; ++i) y[i] = bo::ddm::log_rn(x[i]);
 }

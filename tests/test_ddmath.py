@@ -92,3 +92,39 @@ def test_fast_path_matches_full_precision(ddm_host):
     assert not np.any((okl == 1) & (lg != lg2))
     assert not np.any((oks == 1) & ((s != s2) | (c != c2)))
     assert okl.mean() > 0.999 and oks.mean() > 0.998
+
+
+def test_box_muller_reduction(ddm_host):
+    """sincos_bm_cr(u2) (the generator's reduction of a = fl(2pi u2) through
+    d = u2 - rint(4 u2)/4) equals the full-precision sin / cos of a, and its
+    fast path claims a certain rounding as often as the general one"""
+    import ctypes as C
+    rng = np.random.default_rng(12)
+    n = 2_000_000
+    u = rng.integers(0, 2 ** 53, n, dtype=np.uint64).astype(np.float64) * 2.0 ** -53
+    # quadrant boundaries and their neighbourhoods (a near k pi / 2), both ends
+    edge = []
+    for q in (0.0, 0.125, 0.25, 0.375, 0.5, 0.625, 0.75, 0.875, 1.0):
+        c = round(q * 2 ** 53)
+        edge += [(c + j) * 2.0 ** -53 for j in range(-2000, 2001) if 0 <= c + j < 2 ** 53]
+    u = np.concatenate([u, np.array(edge)])
+    a = 6.283185307179586476925286766559 * u
+    s, c = np.empty_like(u), np.empty_like(u)
+    ok = np.empty(len(u), np.uint8)
+    ub = C.POINTER(C.c_ubyte)
+    ddm_host.ddm_bm_fast_n.argtypes = [C.POINTER(C.c_double)] * 3 + [ub, C.c_long]
+    ddm_host.ddm_bm_cr_n.argtypes = [C.POINTER(C.c_double)] * 3 + [C.c_long]
+    ddm_host.ddm_bm_fast_n(_ptr(u), _ptr(s), _ptr(c), ok.ctypes.data_as(ub), len(u))
+    s2, c2 = np.empty_like(u), np.empty_like(u)
+    ddm_host.ddm_sincos_n(_ptr(a), _ptr(s2), _ptr(c2), len(u))
+    assert not np.any((ok == 1) & ((s != s2) | (c != c2)))
+    assert ok[:n].mean() > 0.998  # (the boundary neighbourhoods fall back more often: cos near 1)
+    s3, c3 = np.empty_like(u), np.empty_like(u)
+    ddm_host.ddm_bm_cr_n(_ptr(u), _ptr(s3), _ptr(c3), len(u))
+    assert np.array_equal(s3, s2) and np.array_equal(c3, c2)
+    # and against mpmath on a sample including the boundary neighbourhoods
+    mp.mp.prec = 160
+    idx = np.concatenate([np.arange(0, n, 997), np.arange(n, len(u), 7)])
+    crs = np.array([float(mp.sin(mp.mpf(float(x)))) for x in a[idx]])
+    crc = np.array([float(mp.cos(mp.mpf(float(x)))) for x in a[idx]])
+    assert np.array_equal(s3[idx], crs) and np.array_equal(c3[idx], crc)
