@@ -219,10 +219,13 @@ BO_DDM_FN double log_fast(double x, bool* ok) {
   P = F(th, P, 1.0 / 3.0);
   const DD p2 = two_prod(th, th);
   const double small = F(M(th, p2.hi), P, S(S(tl, M(0.5, p2.lo)), M(th, tl)));
+  // additions ordered by magnitude (x <= 1, so e <= 0): |e ln2| >= ln 2 > |log c|
+  // for e < 0 (e ln2 = 0 for e = 0), and |e ln2 + log c| >= log(128/127) >
+  // |t| >= |t - t^2/2| unless it is 0 (e = 0, c = 1): quick_two_sum is exact
   const DD el = two_prod((double)e, kLn2Hi);
-  const DD s1 = two_sum(el.hi, lch);
+  const DD s1 = quick_two_sum(el.hi, lch);
   const DD s2 = quick_two_sum(th, M(-0.5, p2.hi));
-  const DD s3 = two_sum(s1.hi, s2.hi);
+  const DD s3 = quick_two_sum(s1.hi, s2.hi);
   double lo = A(s1.lo, s2.lo);
   lo = A(lo, s3.lo);
   lo = A(lo, el.lo);
@@ -261,10 +264,13 @@ BO_DDM_FN void sincos_fast_reduced(DD r, int k, double* sn, double* cs, bool* ok
     s0h = -s0h;
     s0l = -s0l;
   }
-  // sin r = S0 + C0 sin d + S0 (cos d - 1)
+  // sin r = S0 + C0 sin d + S0 (cos d - 1).  The additions are ordered by
+  // magnitude, so the error-free quick_two_sum suffices: for j != 0,
+  // |S0| >= sin(1/64) > |C0 d| (|d| <= 1/128) and |S0 + C0 d| >= sin(1/128) >
+  // |S0 (cos d - 1)|; for j = 0, S0 = 0 (quick_two_sum(0, b) is exact).
   const DD u = two_prod(c0h, dh), v = two_prod(s0h, cmh);
-  DD t1 = two_sum(s0h, u.hi);
-  DD t2 = two_sum(t1.hi, v.hi);
+  DD t1 = quick_two_sum(s0h, u.hi);
+  DD t2 = quick_two_sum(t1.hi, v.hi);
   double lo = A(A(t1.lo, t2.lo), A(u.lo, v.lo));
   lo = A(lo, s0l);
   lo = F(c0h, sdt, lo);
@@ -272,10 +278,10 @@ BO_DDM_FN void sincos_fast_reduced(DD r, int k, double* sn, double* cs, bool* ok
   lo = F(s0h, cml, lo);
   lo = F(s0l, cmh, lo);
   const DD sr = quick_two_sum(t2.hi, lo);
-  // cos r = C0 - S0 sin d + C0 (cos d - 1)
+  // cos r = C0 - S0 sin d + C0 (cos d - 1): C0 >= cos(51/64) > 0.69 dominates
   const DD u2 = two_prod(s0h, dh), v2 = two_prod(c0h, cmh);
-  t1 = two_sum(c0h, -u2.hi);
-  t2 = two_sum(t1.hi, v2.hi);
+  t1 = quick_two_sum(c0h, -u2.hi);
+  t2 = quick_two_sum(t1.hi, v2.hi);
   lo = A(A(t1.lo, t2.lo), S(v2.lo, u2.lo));
   lo = A(lo, c0l);
   lo = F(-s0h, sdt, lo);
