@@ -71,6 +71,9 @@
 #endif
 // Pre-solve passes with a projection range: separate panel (V) and basis (Q)
 // rings, the panel ring deeper (see DEC in pass_kernel); 0: one ring of joint stages
+#ifndef BO_ROWG_RQ_WIDE
+#define BO_ROWG_RQ_WIDE 2  // rows per thread per step of the row-mode Gram at K > 8 (1: 139 -> 2: 131 us at K = 11)
+#endif
 #ifndef BO_DEC_RING
 #define BO_DEC_RING 1
 #endif
@@ -733,7 +736,7 @@ __global__ void __launch_bounds__(pass_threads(UPD, NPRE > 0 && QTX, NPRE > 0 &&
       // warp w consumes tiles w, w + 8, ...; lane l holds rows l + 32 q
       // (q < 4): four independent rows per solve step (ILP, and one shared-
       // memory read of each R entry per four FMAs)
-      constexpr int RQ = KC > 8 ? 1 : 2;  // rows per thread per step (register budget: 168 with 9 warps)
+      constexpr int RQ = KC > 8 ? BO_ROWG_RQ_WIDE : 2;  // rows per thread per step (register budget)
       RingCursor cr(nsub);
       for (int j = 0, it = warp; it < my_tiles; ++j, it += NW, cr.next()) {
         const int s = warp + NW * cr.slot;
