@@ -224,6 +224,12 @@ int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st) {
     const char* e = getenv("BO_MAX_TILE");
     return e ? atoi(e) : 256;
   }();
+  // BO_TILE_PRE: force the tile of the pre-solve passes with a projection range only (diagnostic)
+  static const int tile_pre = [] {
+    const char* e = getenv("BO_TILE_PRE");
+    return e ? atoi(e) : 0;
+  }();
+  int tile_env_k = (tile_pre && ki.npre > 0 && (ki.qtx || ki.upd)) ? tile_pre : tile_env;
   const bool rowg_kind = !r.exact && ki.npre > 0 && ki.gram && !ki.qtx && !ki.upd && ki.sk == SK_NONE &&
                          !ki.store && ki.npost == 0 && (r.K == 6 || r.K == 11);
   int T = 0, NS = 0;
@@ -260,11 +266,11 @@ int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st) {
     for (int want_ns : {want_hi, 2, 1}) {
       for (int tt : {256, 128, 64}) {
         if (T) break;
-        if (want_ns > 2 && tt < 128 && !tile_env) continue;
+        if (want_ns > 2 && tt < 128 && !tile_env_k) continue;
         if (r.exact && tt != 64) continue;
-        if (tile_env && tt != tile_env) continue;
+        if (tile_env_k && tt != tile_env_k) continue;
         if (tt > tile_max) continue;
-        if (rowg_kind && tt != 128 && !tile_env) continue;
+        if (rowg_kind && tt != 128 && !tile_env_k) continue;
         const int S = tile_stride(tt), nsub = tt / tile_sub_rows(tt);
         // row-mode Gram (bo_pass.cuh ROWG): unpadded stages, no X tile
         const bool rowg = rowg_kind && tt == 128;
@@ -311,8 +317,23 @@ int run_pass_single(bo_ctx ctx, PassReq& r, bo_status* st) {
   // buffer: measured on the C2 sequence (scripts/ab_tail.sh), P2_QTX at
   // p = 44 / 55 734 / 810 -> 652 / 737 us and P2_UPD_GRAM_ST 883 / 939 -> 847 /
   // 908 us, while at p <= 33 (3-5 joint stages) they were 3-5% slower.
-  choose(dec_ok && dec_env > 0);
-  if (dec_ok && dec_env == 0 && T && NS <= 2) {
+  // Narrow pre-solve passes (p <= 24): 256-row tiles with decoupled rings.
+  // Their time is a per-tile cost, not bytes, so halving the
+  // tile count pays: measured P1_QTX p = 11 / 22 391 / 455 -> 337 / 389 us,
+  // P1_UPD_GRAM_ST 504 / 562 -> 463 / 512 us (wider ranges lose: one 256-row
+  // basis slot only).
+  static const int t256_maxp = [] {
+    const char* e = getenv("BO_T256_MAXP");
+    return e ? atoi(e) : 24;
+  }();
+  if (dec_ok && dec_env >= 0 && !tile_env_k && r.p <= t256_maxp) {
+    tile_env_k = 256;
+    choose(true);
+    tile_env_k = 0;
+    if (T && NS < 2) T = 0;
+  }
+  if (!T) choose(dec_ok && dec_env > 0);
+  if (dec_ok && dec_env == 0 && T && NS <= 2 && NSV == 0) {
     const int T0 = T, NS0 = NS;
     const size_t r00 = region0, tot0 = total;
     choose(true);
